@@ -1,0 +1,130 @@
+// ref_shim.cpp — C-ABI shim over the UNMODIFIED reference sources, compiled
+// from /root/reference/proj/src by oracle/Makefile into oracle/_ref/.
+// TEST INFRASTRUCTURE ONLY (checker + CPU baseline), never product code.
+//
+// It exposes the reference's own codec (src/codec.cpp:24-95) and its SRA
+// allreduce through SimNet (src/collectives.cpp:475-494) so the tests can
+// validate oracle/cgx_oracle.c against the real thing and bench.py can time
+// the reference CPU path.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "gcomm/codec.hpp"
+#include "gcomm/collectives.hpp"
+#include "gcomm/simnet.hpp"
+#include "gcomm/util.hpp"
+
+namespace {
+thread_local std::string g_err;
+}
+
+extern "C" {
+
+struct ref_segment {
+  std::uint64_t offset, length;
+  std::int32_t mode, bits;
+  std::uint64_t bucket;
+};
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// returns 0 ok, -1 error (message in ref_last_error)
+int ref_quantize(const float* v, std::uint64_t n, int bits, std::uint64_t bucket,
+                 std::uint64_t seed, float* norms, std::uint8_t* packed) {
+  try {
+    gcomm::codec::QuantParams p;
+    p.bits = bits;
+    p.bucket_size = bucket;
+    p.seed = seed;
+    auto c = gcomm::codec::quantize(std::span<const float>(v, n), p);
+    std::memcpy(norms, c.bucket_norms.data(), 4 * c.bucket_norms.size());
+    std::memcpy(packed, c.packed_levels.data(), c.packed_levels.size());
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int ref_dequantize(const float* norms, const std::uint8_t* packed, std::uint64_t n, int bits,
+                   std::uint64_t bucket, float* out) {
+  try {
+    gcomm::codec::CompressedChunk c;
+    c.element_count = n;
+    c.params.bits = bits;
+    c.params.bucket_size = bucket;
+    const std::size_t nb = n ? (n + bucket - 1) / bucket : 0;
+    c.bucket_norms.assign(norms, norms + nb);
+    c.packed_levels.assign(packed, packed + (n * (bits + 1) + 7) / 8);
+    auto v = gcomm::codec::dequantize(c);
+    std::memcpy(out, v.data(), 4 * v.size());
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+std::uint64_t ref_serialize(const float* v, std::uint64_t n, int bits, std::uint64_t bucket,
+                            std::uint64_t seed, std::uint8_t* out) {
+  gcomm::codec::QuantParams p;
+  p.bits = bits;
+  p.bucket_size = bucket;
+  p.seed = seed;
+  auto bytes = gcomm::codec::serialize(gcomm::codec::quantize(std::span<const float>(v, n), p));
+  std::memcpy(out, bytes.data(), bytes.size());
+  return bytes.size();
+}
+
+// SRA allreduce through the reference's SimNet with `nodes` threads.
+// outputs: nodes pointers to d floats. bytes_sent: nodes entries.
+int ref_allreduce(const float* const* inputs, std::uint64_t nodes, std::uint64_t d,
+                  const ref_segment* segs, std::uint64_t nsegs, std::uint64_t step_seed, int op,
+                  float* const* outputs, std::uint64_t* bytes_sent, std::uint64_t* counters) {
+  try {
+    gcomm::collectives::ReduceRequest req;
+    req.inputs.resize(nodes);
+    for (std::uint64_t n = 0; n < nodes; ++n) req.inputs[n].assign(inputs[n], inputs[n] + d);
+    for (std::uint64_t s = 0; s < nsegs; ++s) {
+      gcomm::collectives::Segment seg;
+      seg.offset = segs[s].offset;
+      seg.length = segs[s].length;
+      seg.mode = static_cast<gcomm::model::CodecMode>(segs[s].mode);
+      seg.bits = segs[s].bits;
+      seg.bucket_size = segs[s].bucket;
+      req.segments.push_back(seg);
+    }
+    req.topology = gcomm::collectives::Topology::sra;
+    req.op = op ? gcomm::collectives::ReduceOp::average : gcomm::collectives::ReduceOp::sum;
+    req.step_seed = step_seed;
+    gcomm::simnet::SimNetConfig cfg;
+    cfg.nodes = nodes;
+    gcomm::simnet::SimNet net(cfg);
+    auto res = gcomm::collectives::allreduce(req, net);
+    for (std::uint64_t n = 0; n < nodes; ++n) {
+      std::memcpy(outputs[n], res.outputs[n].data(), 4 * d);
+      if (bytes_sent) bytes_sent[n] = res.trace.bytes_sent[n];
+    }
+    if (counters) {
+      counters[0] = res.trace.compress_calls;
+      counters[1] = res.trace.decompress_calls;
+      counters[2] = res.trace.message_count;
+      counters[3] = res.trace.rounds;
+      counters[4] = res.trace.max_compress_depth;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+std::uint64_t ref_hop_seed(std::uint64_t s, std::uint64_t hop, std::uint64_t node) {
+  return gcomm::collectives::hop_seed(s, hop, node);
+}
+
+}  // extern "C"
