@@ -1,0 +1,140 @@
+/*
+ * gcx.h — C-ABI of the B200-native compressed-allreduce hot path
+ * (libgcx.so, sm_100a).  Plain pointers and sizes only: no torch or C++
+ * types cross this boundary.  Every launcher is asynchronous on the given
+ * CUDA stream (passed as void*; NULL = legacy default stream), never
+ * allocates, and returns 0 on success or a negative GCX_E* code with a
+ * message in gcx_last_error() (thread-local).
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj):
+ *   gcx_quantize        codec::quantize        src/codec.cpp:24-69,  include/gcomm/codec.hpp:50
+ *   gcx_dequantize      codec::dequantize      src/codec.cpp:71-95,  include/gcomm/codec.hpp:51
+ *   gcx_compressed_size codec::compressed_size_bytes src/codec.cpp:151-156
+ *   gcx_encode_pieces   encode_pieces (quantize+serialize per piece)  src/collectives.cpp:143-163
+ *   gcx_decode_pieces   decode_pieces (+ finalize's average)          src/collectives.cpp:165-194, :213-228
+ *   gcx_sra_reduce      run_sra owner step: ascending-id fold, hop-1
+ *                       re-encode, owner decodes its own bytes       src/collectives.cpp:258-292
+ *   gcx_hop_seed        collectives::hop_seed  src/collectives.cpp:29-31
+ *   gcx_uniform01       uniform01              include/gcomm/util.hpp:26-29
+ *
+ * Device payload layout ("message"): a list of pieces, each at a 16-byte
+ * aligned byte offset chosen by the caller.  A quantized piece stores
+ * ceil(len/bucket) f32 norms at `norms` and the (bits+1)-bit LSB-first
+ * packed stream (byte-identical to codec::pack_levels) at `packed`; a raw
+ * piece stores len f32 at `norms` (`packed` unused).  The reference's
+ * 17-byte wire header is not materialised on device: every rank derives the
+ * layout from the segment table, so headers would carry no information.
+ */
+#ifndef GCX_H_
+#define GCX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GCX_OK 0
+#define GCX_E_INVALID (-1)   /* bad parameter (reference: std::invalid_argument) */
+#define GCX_E_CUDA (-2)      /* CUDA launch/runtime failure */
+#define GCX_E_RANGE (-3)     /* payload too short (reference: std::runtime_error) */
+
+/* launch flags (from gcx_plan_tiles) */
+#define GCX_F_BIG_BUCKETS 1u   /* some piece has bucket > GCX_TILE: norm pre-pass */
+#define GCX_F_NEEDS_ZERO 2u    /* some piece's tiles share packed words: zero first */
+#define GCX_F_PIECE_SEEDS 4u   /* use gcx_piece.seed instead of the launch seed */
+
+#define GCX_TILE 4096          /* max elements per CTA tile */
+
+/* One maximal run of a chunk with one codec (collectives.cpp:69-75 Piece). */
+typedef struct gcx_piece {
+  uint64_t src;    /* element offset of the piece in the float buffer it reads/writes */
+  uint64_t len;    /* elements */
+  uint64_t norms;  /* byte offset (from the message base) of the norms / raw f32 payload */
+  uint64_t packed; /* byte offset (from the message base) of the packed stream */
+  uint64_t seed;   /* per-piece seed (only with GCX_F_PIECE_SEEDS) */
+  uint32_t bucket; /* bucket size (quantized pieces) */
+  int32_t bits;    /* 1..8 magnitude bits; 0 = raw f32 (CodecMode::uncompressed) */
+} gcx_piece;
+
+int gcx_version(void);
+const char* gcx_last_error(void);
+
+/* ---- host-side sizing / planning (no GPU needed) ---- */
+uint64_t gcx_compressed_size(uint64_t n, int bits, uint64_t bucket);
+uint64_t gcx_packed_bytes(uint64_t n, int bits);    /* ceil(n*(bits+1)/8) */
+uint64_t gcx_packed_capacity(uint64_t n, int bits); /* rounded up to whole 32-bit words */
+uint64_t gcx_hop_seed(uint64_t step_seed, uint64_t hop, uint64_t node);
+double gcx_uniform01(uint64_t seed, uint64_t a, uint64_t b);
+/* Tile decomposition of a piece table: tile_prefix[npieces+1] (first tile of
+ * each piece, total last) and launch flags.  Returns total tiles or <0. */
+int64_t gcx_plan_tiles(const gcx_piece* pieces, uint32_t npieces, uint32_t* tile_prefix,
+                       uint32_t* flags);
+
+/* ---- single vector codec ----
+ * norms: ceil(n/bucket) f32; packed: gcx_packed_capacity(n,bits) bytes.
+ * bad_key (device u64, may be NULL): atomic-min of the first non-finite input
+ * index; caller presets it to UINT64_MAX and checks it after the stream syncs
+ * (reference message: "non-finite gradient value at index i"). */
+int gcx_quantize(const float* x, uint64_t n, int bits, uint64_t bucket, uint64_t seed,
+                 float* norms, uint8_t* packed, unsigned long long* bad_key, void* stream);
+int gcx_dequantize(const float* norms, const uint8_t* packed, uint64_t n, int bits,
+                   uint64_t bucket, float* out, void* stream);
+
+/* ---- piece-table codec (device tables; tile_prefix from gcx_plan_tiles) ----
+ * encode: src + pieces[k].src ... -> msg + pieces[k].norms/packed.  Raw pieces
+ *         are copied.  bad_key = (piece << 40) | piece-local index.
+ * decode: msg -> dst + pieces[k].src, each value divided by `divisor` when
+ *         divisor != 1 (IEEE f32 division, finalize() average). */
+int gcx_encode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
+                      uint32_t ntiles, uint32_t flags, uint64_t seed, const float* src,
+                      uint8_t* msg, unsigned long long* bad_key, void* stream);
+int gcx_decode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
+                      uint32_t ntiles, const uint8_t* msg, float* dst, float divisor,
+                      void* stream);
+
+/* ---- SRA owner step (fused dequantize-accumulate-requantize) ----
+ * Pieces are chunk-local (src = offset inside the owner's chunk).  The
+ * contribution of node id is `own` when id == me, else the message in recv
+ * slot (id < me ? id : id-1) at recv + slot*slot_stride.  Folds ascending id
+ * in f32, re-encodes with `seed` into bcast, and writes the owner's decoded
+ * result (divided by divisor) to out. */
+int gcx_sra_reduce(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
+                   uint32_t ntiles, uint32_t flags, const uint8_t* recv, uint64_t slot_stride,
+                   const float* own, uint32_t nodes, uint32_t me, uint64_t seed,
+                   uint8_t* bcast, float* out, float divisor, unsigned long long* bad_key,
+                   void* stream);
+
+/* ---- microbenchmarks ----
+ * Integer ceiling of the reference RNG: n draws of uniform01(seed, i/bucket, i),
+ * xor-reduced into *sink (device u64).  variant 0 = reference 64-bit form,
+ * 1 = pipe-balanced split form used by K1/K2, 2 = split form, 2-way ILP. */
+int gcx_hash_bench(uint64_t n, uint64_t seed, uint32_t bucket, int variant,
+                   unsigned long long* sink, void* stream);
+
+/* ---- K4: adaptive-selector statistics (adaptive.cpp:21-97, :390-415) ----
+ * accumulate: sum[i] += (double)v[i]; *nonfinite |= 1 on a non-finite v.
+ * snapshot:   out[i] = (float)sum[i].
+ * reduce:     out[0] = sum_i sum[i]^2, out[1] = sum of the `keep` largest
+ *             squares; scratch >= gcx_stats_scratch_bytes(n).
+ * sq_error:   *out = sum_i (double(a_i) - double(b_i))^2; scratch >= 4736 B. */
+int gcx_stats_accumulate(double* sum, const float* v, uint64_t n, unsigned int* nonfinite,
+                         void* stream);
+int gcx_stats_snapshot(const double* sum, float* out, uint64_t n, void* stream);
+uint64_t gcx_stats_scratch_bytes(uint64_t n);
+int gcx_stats_reduce(const double* sum, uint64_t n, uint64_t keep, void* scratch,
+                     uint64_t scratch_bytes, double* out, void* stream);
+int gcx_sq_error(const float* a, const float* b, uint64_t n, double* scratch, double* out,
+                 void* stream);
+/* mean over nodes, folded in node order then divided by nodes (the adaptive
+ * observation feed, engine.cpp:268-283); stack = nodes rows of n floats */
+int gcx_mean_nodes(const float* stack, uint32_t nodes, uint64_t n, float* out, void* stream);
+const char* gcx_stats_last_error(void);
+
+/* Number of SMs and the kernels' resident CTAs per SM (device 0..). */
+int gcx_device_info(int device, int* sms, int* encode_ctas_per_sm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GCX_H_ */

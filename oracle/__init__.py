@@ -250,6 +250,11 @@ class RefOracle:
                                     C.POINTER(u64)]
         L.ref_hop_seed.restype = u64
         L.ref_hop_seed.argtypes = [u64, u64, u64]
+        L.ref_engine_run.restype = C.c_int
+        L.ref_engine_run.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_char_p), C.POINTER(u64),
+                                     C.POINTER(C.c_int), C.POINTER(flt), C.c_int, u64,
+                                     C.c_char_p, C.c_char_p, u64, u64, C.POINTER(u64),
+                                     C.c_char_p, u64]
 
     def _check(self, rc):
         if rc:
@@ -290,3 +295,34 @@ class RefOracle:
         keys = ["compress_calls", "decompress_calls", "message_count", "rounds",
                 "max_compress_depth"]
         return outs, list(sent), dict(zip(keys, list(ctr)))
+
+    def engine_run(self, nodes, layers, steps, tag, plan_json=None, adaptive_json=None,
+                   step_seed=1, fuse_limit=0):
+        """The reference Engine (src/engine.cpp) over SimNet.  layers: list of
+        (name, elements, kind_int, scale).  -> (per-step digests of node 0's
+        outputs, events JSONL)."""
+        n = len(layers)
+        names = (C.c_char_p * n)(*[x[0].encode() for x in layers])
+        sizes = (C.c_uint64 * n)(*[x[1] for x in layers])
+        kinds = (C.c_int * n)(*[x[2] for x in layers])
+        scales = (C.c_float * n)(*[x[3] for x in layers])
+        dig = (C.c_uint64 * steps)()
+        ev = C.create_string_buffer(1 << 20)
+        self._check(self.lib.ref_engine_run(nodes, n, names, sizes, kinds, scales, steps, tag,
+                                            plan_json.encode() if plan_json else None,
+                                            adaptive_json.encode() if adaptive_json else None,
+                                            step_seed, fuse_limit, dig, ev, 1 << 20))
+        return list(dig), ev.value.decode()
+
+
+def engine_inputs(oracle, layers, nodes, step, tag):
+    """The engine-parity input recipe shared with ref_engine_run: node r,
+    layer t, step k -> scale_t * normal01(H(H(H(tag, k), r), t), i)."""
+    out = []
+    for r in range(nodes):
+        row = []
+        for t, (_, n, _, scale) in enumerate(layers):
+            key = oracle.hash_combine(oracle.hash_combine(oracle.hash_combine(tag, step), r), t)
+            row.append(oracle.normal_vector(n, key, scale))
+        out.append(row)
+    return out

@@ -69,6 +69,33 @@ def sra_cases():
     return cases
 
 
+RESNETISH = [("conv1.w", 9408, 0, 1e-3), ("bn1.w", 64, 2, 1e-2), ("bn1.b", 64, 1, 1e-2),
+             ("layer1.conv.w", 36864, 0, 1e-3), ("layer1.bn.w", 64, 2, 1e-2),
+             ("layer2.conv.w", 73728, 0, 2e-3), ("small.w", 1000, 0, 1e-2),
+             ("fc.w", 20480, 0, 1e-2), ("fc.b", 10, 1, 1e-2)]
+
+
+def engine_cases():
+    plan = json.dumps({"defaults": {"bits": 4, "bucket": 128},
+                       "layers": {"fc.w": {"bits": 8, "bucket": 64},
+                                  "layer2.conv.w": {"bits": 2, "bucket": 512},
+                                  "conv1.w": {"mode": "uncompressed"}}})
+    adaptive = json.dumps({"method": "kmeans", "palette": [2, 4, 8], "stats_period": 3,
+                           "stats_window": 2})
+    linear = json.dumps({"method": "linear", "palette": [2, 3, 4, 5, 6, 8], "stats_period": 2,
+                         "stats_window": 1, "pair_buckets": True})
+    return [
+        dict(name="static_default_n2", nodes=2, layers=RESNETISH, steps=3, tag=0xC2),
+        dict(name="static_default_n5", nodes=5, layers=RESNETISH, steps=2, tag=0xC3),
+        dict(name="static_plan_n4_small_fuse", nodes=4, layers=RESNETISH, steps=3, tag=0xC4,
+             plan=plan, fuse_limit=200000, step_seed=99),
+        dict(name="adaptive_kmeans_n3", nodes=3, layers=RESNETISH, steps=5, tag=0xC5,
+             adaptive=adaptive),
+        dict(name="adaptive_linear_pairs_n2", nodes=2, layers=RESNETISH, steps=4, tag=0xC6,
+             adaptive=linear),
+    ]
+
+
 def main():
     ref = RefOracle()
     o = Oracle()
@@ -102,7 +129,18 @@ def main():
     with open(os.path.join(OUT, "sra.json"), "w") as f:
         json.dump(dict(source="compiled reference src/collectives.cpp run_sra via SimNet",
                        cases=sra), f, indent=0)
-    print(f"wrote {len(codec)} codec and {len(sra)} sra cases to {OUT}")
+    eng = []
+    for c in engine_cases():
+        dig, ev = ref.engine_run(c["nodes"], c["layers"], c["steps"], c["tag"], c.get("plan"),
+                                 c.get("adaptive"), c.get("step_seed", 1), c.get("fuse_limit", 0))
+        swaps = [json.loads(x) for x in ev.splitlines()]
+        c.update(digests=dig, plan_swaps=[[e["step"], e["payload"]["bits"]] for e in swaps
+                                          if e["event"] == "plan_swap"])
+        eng.append(c)
+    with open(os.path.join(OUT, "engine.json"), "w") as f:
+        json.dump(dict(source="compiled reference src/engine.cpp via SimNet (oracle/_ref)",
+                       cases=eng), f, indent=0)
+    print(f"wrote {len(codec)} codec, {len(sra)} sra, {len(eng)} engine cases to {OUT}")
 
 
 if __name__ == "__main__":

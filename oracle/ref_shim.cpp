@@ -128,3 +128,69 @@ std::uint64_t ref_hop_seed(std::uint64_t s, std::uint64_t hop, std::uint64_t nod
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Engine (src/engine.cpp) through SimNet, for end-to-end engine / adaptive
+// parity.  Inputs: node r, layer t, step k get
+//   scales[t] * normal01(hash_combine(hash_combine(hash_combine(tag, k), r), t), i).
+// digests[k] = FNV-1a of node 0's outputs of step k, layers concatenated
+// (all nodes are checked identical).  events: the engine's JSONL log.
+// ---------------------------------------------------------------------------
+#include "gcomm/engine.hpp"
+
+extern "C" int ref_engine_run(int nodes, int nlayers, const char** names, const std::uint64_t* sizes,
+                              const int* kinds, const float* scales, int steps, std::uint64_t tag,
+                              const char* plan_json, const char* adaptive_json,
+                              std::uint64_t step_seed, std::uint64_t fuse_limit,
+                              std::uint64_t* digests, char* events, std::uint64_t events_cap) {
+  try {
+    using namespace gcomm;
+    engine::EngineConfig cfg;
+    cfg.nodes = nodes;
+    cfg.step_seed = step_seed;
+    if (fuse_limit) cfg.fuse_limit_bytes = fuse_limit;
+    if (plan_json && *plan_json) cfg.plan = model::CompressionPlan::from_json(plan_json);
+    if (adaptive_json && *adaptive_json) {
+      cfg.plan_source = engine::PlanSource::adaptive;
+      cfg.adaptive = adaptive::AdaptiveConfig::from_json(adaptive_json);
+    }
+    simnet::SimNetConfig net;
+    net.nodes = nodes;
+    engine::Engine eng(cfg, net);
+    for (int k = 0; k < steps; ++k) {
+      for (int r = 0; r < nodes; ++r)
+        for (int t = 0; t < nlayers; ++t) {
+          model::GradientTensor g;
+          g.layer.name = names[t];
+          g.layer.elements = sizes[t];
+          g.layer.kind = static_cast<model::LayerKind>(kinds[t]);
+          g.values.resize(sizes[t]);
+          const std::uint64_t key = hash_combine(hash_combine(hash_combine(tag, k), r), t);
+          for (std::uint64_t i = 0; i < sizes[t]; ++i) g.values[i] = scales[t] * normal01(key, i);
+          eng.submit(r, std::move(g));
+        }
+      std::vector<std::uint8_t> bytes0;
+      for (int r = 0; r < nodes; ++r) {
+        auto out = eng.flush(r);
+        std::vector<std::uint8_t> bytes;
+        for (const auto& g : out) {
+          const auto* p = reinterpret_cast<const std::uint8_t*>(g.values.data());
+          bytes.insert(bytes.end(), p, p + 4 * g.values.size());
+        }
+        if (r == 0) bytes0 = std::move(bytes);
+        else if (bytes != bytes0) throw std::runtime_error("replicas disagree");
+      }
+      digests[k] = fnv1a64(bytes0);
+    }
+    const std::string ev = eng.events_json();
+    if (events && events_cap) {
+      const std::size_t n = std::min<std::size_t>(ev.size(), events_cap - 1);
+      std::memcpy(events, ev.data(), n);
+      events[n] = 0;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}

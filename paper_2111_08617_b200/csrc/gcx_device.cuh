@@ -1,0 +1,160 @@
+// gcx_device.cuh — bit-exact device arithmetic for the CGX codec on sm_100a.
+//
+// Everything here reproduces the reference's FP64/integer semantics
+// (/root/reference/proj/src/codec.cpp:24-95, include/gcomm/util.hpp:14-29)
+// WITHOUT the XU-pipe conversion instructions (F2F/I2F/F2I), which the first
+// ncu capture showed saturating the XU pipe at 193% of peak.  Conversions are
+// rebuilt from integer/FP64 pipe operations; each trick is exact and checked
+// bit-for-bit against the oracle by tests/test_gpu_codec.py.
+#pragma once
+
+#include <cstdint>
+
+namespace gcx_dev {
+
+// |v| as an exact double: float exponent rebias in the integer pipes.  Zero
+// and subnormals (exponent field 0) take the slow conversion.
+__device__ __forceinline__ double f32abs_to_f64(uint32_t u_abs) {
+  double d = __hiloint2double(int((u_abs >> 3) + 0x38000000u), int(u_abs << 29));
+  if (u_abs < 0x00800000u) d = u_abs == 0 ? 0.0 : double(__uint_as_float(u_abs));
+  return d;
+}
+
+// RN-even double -> float for a non-negative finite q below 2^128; results
+// below the normal float range take the slow conversion.
+__device__ __forceinline__ float f64pos_to_f32_rn(double q) {
+  const unsigned long long D = __double_as_longlong(q);
+  if (D < 0x3810000000000000ull) return __double2float_rn(q);
+  const unsigned long long R = D + 0x0FFFFFFFull + ((D >> 29) & 1ull);
+  return __uint_as_float(uint32_t(R >> 29) - (896u << 23));
+}
+
+// small non-negative integer (< 2^31) as an exact double
+__device__ __forceinline__ double u32_to_f64(uint32_t k) {
+  return __dsub_rn(__hiloint2double(0x43300000, int(k)), 4503599627370496.0);
+}
+
+// ---------------------------------------------------------------------------
+// mix64 (util.hpp:14-19) on (lo, hi) 32-bit halves.  The reference form
+// compiles to ~27 ops per call, ~2/3 of them on the ALU pipe (SHF/LOP3/
+// IADD3).  Here the high-word right shifts are done as IMAD.HI with an opaque
+// power-of-two multiplier so they issue on the FMA pipe instead, balancing
+// the two pipes.  `Opq` carries the multipliers in registers ptxas cannot
+// constant-fold back into shifts.
+// ---------------------------------------------------------------------------
+struct Opq {
+  uint32_t m30, m27, m31;  // 2^(32-k): hi >> k == mulhi(hi, 2^(32-k))
+};
+
+__device__ __forceinline__ Opq make_opq() {
+  Opq o{4u, 32u, 2u};
+  asm volatile("" : "+r"(o.m30), "+r"(o.m27), "+r"(o.m31));
+  return o;
+}
+
+// z ^= z >> k  with hi >> k on the FMA pipe
+__device__ __forceinline__ void xorshift(uint32_t& lo, uint32_t& hi, uint32_t k, uint32_t mk) {
+  const uint32_t f = __funnelshift_r(lo, hi, k);  // (z >> k).lo  [ALU]
+  const uint32_t t = __umulhi(hi, mk);            // (z >> k).hi  [FMA]
+  lo ^= f;
+  hi ^= t;
+}
+
+// z *= C (mod 2^64): 3 FMA-pipe ops
+__device__ __forceinline__ void mul64c(uint32_t& lo, uint32_t& hi, uint32_t cl, uint32_t ch) {
+  const unsigned long long w = (unsigned long long)lo * cl;
+  uint32_t nhi = uint32_t(w >> 32);
+  nhi += lo * ch;
+  nhi += hi * cl;
+  lo = uint32_t(w);
+  hi = nhi;
+}
+
+__device__ __forceinline__ void mix64_split(uint32_t& lo, uint32_t& hi, const Opq& o) {
+  // z += 0x9e3779b97f4a7c15
+  asm("add.cc.u32 %0, %0, 0x7f4a7c15;\n\taddc.u32 %1, %1, 0x9e3779b9;" : "+r"(lo), "+r"(hi));
+  xorshift(lo, hi, 30, o.m30);
+  mul64c(lo, hi, 0x1ce4e5b9u, 0xbf58476du);
+  xorshift(lo, hi, 27, o.m27);
+  mul64c(lo, hi, 0x133111ebu, 0x94d049bbu);
+  xorshift(lo, hi, 31, o.m31);
+}
+
+// h = mix64(seed ^ mix64(b ^ mix64(i)))  (uniform01's key, util.hpp:26-29)
+__device__ __forceinline__ void draw_key(uint32_t i_lo, uint32_t i_hi, uint32_t b_lo, uint32_t b_hi,
+                                         uint32_t s_lo, uint32_t s_hi, const Opq& o,
+                                         uint32_t& h_lo, uint32_t& h_hi) {
+  uint32_t lo = i_lo, hi = i_hi;
+  mix64_split(lo, hi, o);
+  lo ^= b_lo;
+  hi ^= b_hi;
+  mix64_split(lo, hi, o);
+  lo ^= s_lo;
+  hi ^= s_hi;
+  mix64_split(lo, hi, o);
+  h_lo = lo;
+  h_hi = hi;
+}
+
+// reference form, for the microbenchmark and as documentation
+__device__ __forceinline__ uint64_t mix64_ref(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// ---------------------------------------------------------------------------
+// One element of codec::quantize (codec.cpp:50-64), branch-free so two
+// elements interleave.  nd = (double)norm, y = RN(1/norm), sd = s.
+// Returns the (bits+1)-bit field level | sign << bits.
+//   a  = RN(|v|/norm)   : q0 = |v|*y; r = fma(-nd, q0, |v|) (exact);
+//                         a = fma(r, y, q0)  (correctly rounded, see header)
+//   x  = RN(a*s); level = trunc(x) via RZ(x + 2^52); p = x - level (exact)
+//   up = uniform01 < p  <=>  (k53 >> 1) < (k53 odd ? p*2^52 - 1/2 : p*2^52)
+//        with k53 = h >> 11; both sides exact doubles
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t quantize_field(uint32_t u, double nd, double y, double sd,
+                                                   uint32_t s, int bits, uint32_t h_lo,
+                                                   uint32_t h_hi) {
+  const double av = f32abs_to_f64(u & 0x7FFFFFFFu);
+  const double q0 = __dmul_rn(av, y);
+  const double r = __fma_rn(-nd, q0, av);
+  const double a = __fma_rn(r, y, q0);
+  const double x = __dmul_rn(a, sd);
+  const double t = __dadd_rz(x, 4503599627370496.0);  // 2^52 + trunc(x)
+  uint32_t level = uint32_t(__double2loint(t));
+  const double lv = __dsub_rn(t, 4503599627370496.0);
+  const double p = __dsub_rn(x, lv);
+  const double Q = __dmul_rn(p, 4503599627370496.0);
+  // kd = (h >> 12) as an exact double
+  const uint32_t k_lo = __funnelshift_r(h_lo, h_hi, 12);
+  const uint32_t k_hi = (h_hi >> 12) | 0x43300000u;
+  const double kd = __dsub_rn(__hiloint2double(int(k_hi), int(k_lo)), 4503599627370496.0);
+  const double thr = (h_lo & 0x800u) ? __dsub_rn(Q, 0.5) : Q;
+  const uint32_t up = kd < thr ? 1u : 0u;
+  level = level >= s ? s : level + up;
+  return level | ((u >> 31) << bits);
+}
+
+// codec.cpp:84-93: level 0 -> +0.0f; else RN32(RN64(RN64(norm*l)/s)), signed.
+// norm_d = (double)norm, ys = RN(1/s), sd = s.
+__device__ __forceinline__ float dequant_field(double norm_d, uint32_t level, uint32_t sign,
+                                               double sd, double ys) {
+  const double nl = __dmul_rn(norm_d, u32_to_f64(level));  // exact: <= 32 significant bits
+  const double q0 = __dmul_rn(nl, ys);
+  const double r = __fma_rn(-sd, q0, nl);
+  const double q = __fma_rn(r, ys, q0);
+  const float mag = level == 0 ? 0.0f : f64pos_to_f32_rn(q);
+  return (sign && level) ? -mag : mag;
+}
+
+// finalize's average (collectives.cpp:223-227): v / (float)N, exactly.
+// N a power of two: multiplying by the exact reciprocal is the same real
+// number, hence the same rounding; otherwise IEEE division.
+__device__ __forceinline__ float apply_divisor(float v, float divisor, float recip, bool pow2) {
+  if (divisor == 1.0f) return v;
+  return pow2 ? __fmul_rn(v, recip) : __fdiv_rn(v, divisor);
+}
+
+}  // namespace gcx_dev

@@ -1,0 +1,592 @@
+// collectives.cpp — compressed SRA allreduce on B200.
+// Reference: /root/reference/proj/src/collectives.cpp (run_sra :230-310,
+// chunk_boundaries :106-122, pieces_for :124-140, finalize :213-228,
+// allreduce :475-494).  Two drivers share the layout code:
+//   allreduce(request, nodes)  all nodes on the current GPU (drop-in for the
+//                              reference's single-process allreduce(req, net))
+//   DeviceReducer              one rank per GPU, NCCL grouped send/recv over
+//                              NVLink for the two exchange rounds.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "devmem.hpp"
+#include "gcomm.hpp"
+
+namespace gcomm::collectives {
+
+using detail::align_up;
+using detail::cuda_check;
+using detail::DeviceBuffer;
+
+namespace {
+
+void gcx_check(int rc) {
+  if (rc == GCX_E_INVALID) throw std::invalid_argument(gcx_last_error());
+  if (rc != GCX_OK) throw std::runtime_error(gcx_last_error());
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw std::runtime_error(std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+constexpr std::uint64_t kMsgAlign = 256;
+
+}  // namespace
+
+Topology topology_from_string(const std::string& s) {
+  if (s == "sra") return Topology::sra;
+  if (s == "ring") return Topology::ring;
+  if (s == "tree") return Topology::tree;
+  throw std::invalid_argument("unknown topology: " + s);
+}
+
+std::string to_string(Topology topology) {
+  switch (topology) {
+    case Topology::sra: return "sra";
+    case Topology::ring: return "ring";
+    case Topology::tree: return "tree";
+  }
+  return "sra";
+}
+
+// collectives.cpp:29-31
+std::uint64_t hop_seed(std::uint64_t step_seed, std::uint64_t hop, std::uint64_t node) {
+  return hash_combine(step_seed, hash_combine(hop, node));
+}
+
+// collectives.cpp:33-45
+std::uint64_t latency_rounds(Topology topology, std::size_t nodes) {
+  if (nodes <= 1) return 0;
+  switch (topology) {
+    case Topology::sra: return 2;
+    case Topology::ring: return 2 * (nodes - 1);
+    case Topology::tree: {
+      std::size_t levels = 0;
+      while ((std::size_t{1} << levels) < nodes) ++levels;
+      return 2 * levels;
+    }
+  }
+  return 0;
+}
+
+std::uint64_t StepTrace::total_bytes_sent() const {
+  std::uint64_t t = 0;
+  for (auto b : bytes_sent) t += b;
+  return t;
+}
+
+std::uint64_t StepTrace::total_bytes_received() const {
+  std::uint64_t t = 0;
+  for (auto b : bytes_received) t += b;
+  return t;
+}
+
+void StepTrace::accumulate(const StepTrace& o) {
+  if (bytes_sent.size() < o.bytes_sent.size()) bytes_sent.resize(o.bytes_sent.size(), 0);
+  if (bytes_received.size() < o.bytes_received.size())
+    bytes_received.resize(o.bytes_received.size(), 0);
+  for (std::size_t i = 0; i < o.bytes_sent.size(); ++i) bytes_sent[i] += o.bytes_sent[i];
+  for (std::size_t i = 0; i < o.bytes_received.size(); ++i)
+    bytes_received[i] += o.bytes_received[i];
+  message_count += o.message_count;
+  rounds += o.rounds;
+  device_time_s += o.device_time_s;
+  compress_calls += o.compress_calls;
+  decompress_calls += o.decompress_calls;
+  max_compress_depth = std::max(max_compress_depth, o.max_compress_depth);
+  device_bytes_sent += o.device_bytes_sent;
+}
+
+// collectives.cpp:77-102 (same messages)
+void validate_request(const ReduceRequest& req, std::size_t nodes) {
+  if (req.inputs.size() != nodes)
+    throw std::invalid_argument("expected one input buffer per node");
+  const std::size_t d = req.inputs.empty() ? 0 : req.inputs[0].size();
+  for (const auto& in : req.inputs)
+    if (in.size() != d) throw std::invalid_argument("input buffers must have equal lengths");
+  std::size_t cursor = 0;
+  for (const auto& seg : req.segments) {
+    if (seg.offset != cursor)
+      throw std::invalid_argument("segments must cover the buffer contiguously");
+    if (seg.length == 0) throw std::invalid_argument("zero-length segment");
+    if (seg.mode == model::CodecMode::topk)
+      throw std::invalid_argument("topk segments use the sparse path");
+    if (seg.mode == model::CodecMode::quantize) {
+      codec::QuantParams p;
+      p.bits = seg.bits;
+      p.bucket_size = seg.bucket_size;
+      p.validate();
+      if (seg.bucket_size > 0xFFFFFFFFull)
+        throw std::invalid_argument("bucket size must fit 32 bits");
+    }
+    cursor += seg.length;
+  }
+  if (cursor != d)
+    throw std::invalid_argument("segments cover " + std::to_string(cursor) +
+                                " elements but buffers hold " + std::to_string(d));
+}
+
+// collectives.cpp:106-122
+std::vector<std::size_t> chunk_boundaries(std::size_t d, std::size_t nodes,
+                                          const std::vector<Segment>& segments) {
+  std::vector<std::size_t> bounds(nodes + 1, 0);
+  bounds[nodes] = d;
+  for (std::size_t k = 1; k < nodes; ++k) {
+    std::size_t p = d * k / nodes;
+    for (const auto& seg : segments) {
+      if (p >= seg.offset && p < seg.offset + seg.length) {
+        if (seg.mode == model::CodecMode::quantize)
+          p = seg.offset + ((p - seg.offset) / seg.bucket_size) * seg.bucket_size;
+        break;
+      }
+    }
+    bounds[k] = std::max(bounds[k - 1], p);
+  }
+  return bounds;
+}
+
+// pieces_for (collectives.cpp:124-140) + the device payload layout of a
+// chunk message: 16-byte aligned norms / packed / raw regions per piece.
+SraLayout make_layout(std::size_t d, std::size_t nodes, const std::vector<Segment>& segments) {
+  SraLayout L;
+  L.d = d;
+  L.nodes = nodes;
+  L.bounds = chunk_boundaries(d, nodes, segments);
+  L.chunks.resize(nodes);
+  L.gather_offset.resize(nodes);
+  std::uint64_t goff = 0;
+  for (std::size_t c = 0; c < nodes; ++c) {
+    ChunkLayout& ch = L.chunks[c];
+    ch.lo = L.bounds[c];
+    ch.hi = L.bounds[c + 1];
+    std::uint64_t off = 0;
+    for (const auto& seg : segments) {
+      const std::size_t a = std::max(ch.lo, seg.offset);
+      const std::size_t b = std::min(ch.hi, seg.offset + seg.length);
+      if (a >= b) continue;
+      gcx_piece p{};
+      p.src = a;
+      p.len = b - a;
+      if (seg.mode == model::CodecMode::quantize) {
+        p.bits = seg.bits;
+        p.bucket = std::uint32_t(seg.bucket_size);
+        p.norms = off;
+        const std::uint64_t nb = (p.len + seg.bucket_size - 1) / seg.bucket_size;
+        p.packed = align_up(off + 4 * nb, 16);
+        off = align_up(p.packed + gcx_packed_capacity(p.len, p.bits), 16);
+        ch.wire_bytes += 17 + gcx_compressed_size(p.len, p.bits, seg.bucket_size);
+        ch.quantized_pieces += 1;
+      } else {
+        p.bits = 0;
+        p.bucket = 0;
+        p.norms = off;
+        p.packed = off;
+        off = align_up(off + 4 * p.len, 16);
+        ch.wire_bytes += 4 * p.len;
+      }
+      ch.pieces.push_back(p);
+    }
+    ch.msg_bytes = off;
+    L.gather_offset[c] = goff;
+    goff += align_up(off, kMsgAlign);
+  }
+  L.gather_bytes = goff;
+  return L;
+}
+
+// Reference-equivalent accounting of one SRA step (simnet.hpp:43-57 as
+// run_sra fills it): wire bytes with 17-byte headers, 2N(N-1) messages.
+StepTrace sra_trace(const SraLayout& L) {
+  StepTrace t;
+  const std::size_t N = L.nodes;
+  t.bytes_sent.assign(N, 0);
+  t.bytes_received.assign(N, 0);
+  if (N <= 1) return t;
+  std::uint64_t q_total = 0, all_wire = 0;
+  bool any_q = false;
+  for (const auto& ch : L.chunks) {
+    q_total += ch.quantized_pieces;
+    all_wire += ch.wire_bytes;
+    any_q = any_q || ch.any_quantized();
+  }
+  for (std::size_t me = 0; me < N; ++me) {
+    const std::uint64_t mine = L.chunks[me].wire_bytes;
+    t.bytes_sent[me] = (all_wire - mine) + (N - 1) * mine;
+    t.bytes_received[me] = (N - 1) * mine + (all_wire - mine);
+  }
+  t.message_count = 2 * N * (N - 1);
+  t.rounds = 2;
+  t.compress_calls = N * q_total;
+  t.decompress_calls = (2 * N - 1) * q_total;
+  t.max_compress_depth = any_q ? 2 : 0;
+  for (std::size_t me = 0; me < N; ++me) {
+    std::uint64_t dev = 0;
+    for (std::size_t c = 0; c < N; ++c)
+      if (c != me) dev += L.chunks[c].msg_bytes + L.chunks[me].msg_bytes;
+    t.device_bytes_sent += dev;
+  }
+  return t;
+}
+
+namespace {
+
+// A device piece table with its tile prefix, uploaded into one blob.
+struct Table {
+  std::vector<gcx_piece> pieces;
+  std::vector<std::uint32_t> prefix;
+  std::uint32_t ntiles = 0;
+  std::uint32_t flags = 0;
+  std::size_t dev_off = 0;  // byte offset of the pieces in the blob
+  std::size_t pre_off = 0;
+  void plan() {
+    prefix.assign(pieces.size() + 1, 0);
+    const std::int64_t nt =
+        gcx_plan_tiles(pieces.data(), std::uint32_t(pieces.size()), prefix.data(), &flags);
+    if (nt < 0) gcx_check(int(nt));
+    ntiles = std::uint32_t(nt);
+  }
+};
+
+struct TableBlob {
+  DeviceBuffer buf;
+  void upload(std::vector<Table*> tables) {
+    std::size_t off = 0;
+    for (Table* t : tables) {
+      t->dev_off = off;
+      off = align_up(off + sizeof(gcx_piece) * std::max<std::size_t>(1, t->pieces.size()), 16);
+      t->pre_off = off;
+      off = align_up(off + 4 * t->prefix.size(), 16);
+    }
+    std::vector<std::uint8_t> host(off, 0);
+    for (Table* t : tables) {
+      if (!t->pieces.empty())
+        std::memcpy(host.data() + t->dev_off, t->pieces.data(), sizeof(gcx_piece) * t->pieces.size());
+      std::memcpy(host.data() + t->pre_off, t->prefix.data(), 4 * t->prefix.size());
+    }
+    buf.reset(off);
+    cuda_check(cudaMemcpy(buf.get(), host.data(), off, cudaMemcpyHostToDevice), "table upload");
+  }
+  const gcx_piece* pieces(const Table& t) const {
+    return reinterpret_cast<const gcx_piece*>(buf.get<std::uint8_t>() + t.dev_off);
+  }
+  const std::uint32_t* prefix(const Table& t) const {
+    return reinterpret_cast<const std::uint32_t*>(buf.get<std::uint8_t>() + t.pre_off);
+  }
+};
+
+Table shifted(const std::vector<gcx_piece>& src, std::uint64_t delta) {
+  Table t;
+  t.pieces = src;
+  for (auto& p : t.pieces) {
+    p.norms += delta;
+    p.packed += delta;
+  }
+  return t;
+}
+
+void append(Table& t, const std::vector<gcx_piece>& src, std::uint64_t delta) {
+  for (gcx_piece p : src) {
+    p.norms += delta;
+    p.packed += delta;
+    t.pieces.push_back(p);
+  }
+}
+
+[[noreturn]] void throw_non_finite(const Table& t, std::uint64_t key) {
+  const std::uint64_t local = key & ((1ULL << 40) - 1);
+  (void)t;
+  throw std::invalid_argument("non-finite gradient value at index " + std::to_string(local));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// all nodes on one GPU
+// ---------------------------------------------------------------------------
+ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
+  if (nodes < 1) throw std::invalid_argument("simnet needs at least one node");
+  if (nodes > 64) throw std::invalid_argument("simnet supports at most 64 nodes");
+  validate_request(req, nodes);
+  ReduceResult result;
+  if (nodes == 1) {  // collectives.cpp:479-486: identity, nothing compressed
+    result.outputs = req.inputs;
+    result.trace.bytes_sent.assign(1, 0);
+    result.trace.bytes_received.assign(1, 0);
+    return result;
+  }
+  if (req.topology != Topology::sra)
+    throw std::invalid_argument("topology " + to_string(req.topology) +
+                                " is not on the B200 path (sra only)");
+  detail::require_device();
+  const std::size_t N = nodes, d = req.inputs[0].size();
+  const SraLayout L = make_layout(d, N, req.segments);
+
+  // mailbox arena: chunk c holds N-1 slots of stride S_c (one per sender)
+  std::vector<std::uint64_t> slot_stride(N), mbase(N);
+  std::uint64_t arena = 0;
+  for (std::size_t c = 0; c < N; ++c) {
+    slot_stride[c] = align_up(std::max<std::uint64_t>(L.chunks[c].msg_bytes, 16), kMsgAlign);
+    mbase[c] = arena;
+    arena += slot_stride[c] * (N - 1);
+  }
+  std::vector<Table> send(N), own(N), dec(N);
+  std::uint32_t flags = 0;
+  for (std::size_t id = 0; id < N; ++id) {
+    for (std::size_t c = 0; c < N; ++c) {
+      if (c == id) continue;
+      const std::uint64_t slot = id < c ? id : id - 1;
+      append(send[id], L.chunks[c].pieces, mbase[c] + slot * slot_stride[c]);
+      append(dec[id], L.chunks[c].pieces, L.gather_offset[c]);
+    }
+    own[id] = shifted(L.chunks[id].pieces, 0);
+    send[id].plan();
+    own[id].plan();
+    dec[id].plan();
+    flags |= send[id].flags | own[id].flags;
+  }
+  std::vector<Table*> all;
+  for (std::size_t k = 0; k < N; ++k) {
+    all.push_back(&send[k]);
+    all.push_back(&own[k]);
+    all.push_back(&dec[k]);
+  }
+  TableBlob blob;
+  blob.upload(all);
+
+  detail::Stream stream;
+  cudaStream_t st = stream.get();
+  DeviceBuffer in(4 * d * N + 16), out(4 * d * N + 16), mail(arena + 16),
+      gather(L.gather_bytes + 16), bad(16 * N);
+  for (std::size_t k = 0; k < N; ++k)
+    cuda_check(cudaMemcpyAsync(in.get<float>() + k * d, req.inputs[k].data(), 4 * d,
+                               cudaMemcpyHostToDevice, st), "H2D");
+  cuda_check(cudaMemsetAsync(bad.get(), 0xFF, 16 * N, st), "memset");
+  if (flags & GCX_F_NEEDS_ZERO) {
+    cuda_check(cudaMemsetAsync(mail.get(), 0, mail.size(), st), "memset");
+    cuda_check(cudaMemsetAsync(gather.get(), 0, gather.size(), st), "memset");
+  }
+  cudaEvent_t e0, e1;
+  cuda_check(cudaEventCreate(&e0), "event");
+  cuda_check(cudaEventCreate(&e1), "event");
+  cudaEventRecord(e0, st);
+  auto* badp = bad.get<unsigned long long>();
+  const float divisor = req.op == ReduceOp::average ? float(N) : 1.0f;
+  // stage 1 (scatter): every sender encodes its share of every other chunk
+  for (std::size_t id = 0; id < N; ++id)
+    gcx_check(gcx_encode_pieces(blob.pieces(send[id]), blob.prefix(send[id]),
+                                std::uint32_t(send[id].pieces.size()), send[id].ntiles,
+                                send[id].flags, hop_seed(req.step_seed, 0, id),
+                                in.get<float>() + id * d, mail.get<std::uint8_t>(), badp + id, st));
+  // owners: ascending-id fold, hop-1 re-encode, decode own bytes
+  for (std::size_t c = 0; c < N; ++c)
+    gcx_check(gcx_sra_reduce(blob.pieces(own[c]), blob.prefix(own[c]),
+                             std::uint32_t(own[c].pieces.size()), own[c].ntiles, own[c].flags,
+                             mail.get<std::uint8_t>() + mbase[c], slot_stride[c],
+                             in.get<float>() + c * d, std::uint32_t(N), std::uint32_t(c),
+                             hop_seed(req.step_seed, 1, c),
+                             gather.get<std::uint8_t>() + L.gather_offset[c],
+                             out.get<float>() + c * d, divisor, badp + N + c, st));
+  // stage 2 (all-gather): everyone decodes the other owners' bytes
+  for (std::size_t id = 0; id < N; ++id)
+    gcx_check(gcx_decode_pieces(blob.pieces(dec[id]), blob.prefix(dec[id]),
+                                std::uint32_t(dec[id].pieces.size()), dec[id].ntiles,
+                                gather.get<std::uint8_t>(), out.get<float>() + id * d, divisor, st));
+  cudaEventRecord(e1, st);
+  result.outputs.assign(N, std::vector<float>(d));
+  for (std::size_t k = 0; k < N; ++k)
+    cuda_check(cudaMemcpyAsync(result.outputs[k].data(), out.get<float>() + k * d, 4 * d,
+                               cudaMemcpyDeviceToHost, st), "D2H");
+  std::vector<std::uint64_t> badh(2 * N);
+  cuda_check(cudaMemcpyAsync(badh.data(), bad.get(), 16 * N, cudaMemcpyDeviceToHost, st), "D2H");
+  stream.sync();
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  for (std::size_t k = 0; k < 2 * N; ++k)
+    if (badh[k] != ~0ULL) throw_non_finite(k < N ? send[k] : own[k - N], badh[k]);
+  result.trace = sra_trace(L);
+  result.trace.device_time_s = ms * 1e-3;
+  return result;
+}
+
+// ---------------------------------------------------------------------------
+// one rank per GPU over NCCL
+// ---------------------------------------------------------------------------
+std::vector<std::uint8_t> Communicator::unique_id() {
+  ncclUniqueId id;
+  nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+  return std::vector<std::uint8_t>(reinterpret_cast<std::uint8_t*>(&id),
+                                   reinterpret_cast<std::uint8_t*>(&id) + sizeof(id));
+}
+
+Communicator::Communicator(int rank, int nranks, const std::vector<std::uint8_t>& id)
+    : rank_(rank), nranks_(nranks) {
+  if (id.size() != sizeof(ncclUniqueId)) throw std::invalid_argument("bad NCCL unique id size");
+  detail::require_device();
+  ncclUniqueId uid;
+  std::memcpy(&uid, id.data(), sizeof(uid));
+  ncclComm_t comm;
+  nccl_check(ncclCommInitRank(&comm, nranks, uid, rank), "ncclCommInitRank");
+  comm_ = comm;
+}
+
+Communicator::~Communicator() {
+  if (comm_) ncclCommDestroy(static_cast<ncclComm_t>(comm_));
+}
+
+struct DeviceReducer::Impl {
+  Table send, own, dec;
+  TableBlob blob;
+  DeviceBuffer send_buf, recv_buf, gather_buf, bad;
+  std::uint64_t recv_stride = 0;
+  std::uint32_t flags = 0;
+};
+
+DeviceReducer::DeviceReducer(Communicator& comm, std::size_t d, std::vector<Segment> segments)
+    : comm_(comm), impl_(std::make_unique<Impl>()) {
+  ReduceRequest probe;
+  probe.segments = segments;
+  probe.inputs.assign(1, {});
+  // validate the segment table without materialising inputs
+  std::size_t cursor = 0;
+  for (const auto& seg : segments) {
+    if (seg.offset != cursor)
+      throw std::invalid_argument("segments must cover the buffer contiguously");
+    if (seg.length == 0) throw std::invalid_argument("zero-length segment");
+    if (seg.mode == model::CodecMode::topk)
+      throw std::invalid_argument("topk segments use the sparse path");
+    if (seg.mode == model::CodecMode::quantize) {
+      codec::QuantParams p;
+      p.bits = seg.bits;
+      p.bucket_size = seg.bucket_size;
+      p.validate();
+    }
+    cursor += seg.length;
+  }
+  if (cursor != d)
+    throw std::invalid_argument("segments cover " + std::to_string(cursor) +
+                                " elements but buffers hold " + std::to_string(d));
+  const std::size_t N = std::size_t(comm.size()), me = std::size_t(comm.rank());
+  layout_ = make_layout(d, N, segments);
+  if (N == 1) return;
+  Impl& I = *impl_;
+  for (std::size_t c = 0; c < N; ++c) {
+    if (c == me) continue;
+    append(I.send, layout_.chunks[c].pieces, layout_.gather_offset[c]);
+    append(I.dec, layout_.chunks[c].pieces, layout_.gather_offset[c]);
+  }
+  I.own = shifted(layout_.chunks[me].pieces, 0);
+  I.send.plan();
+  I.own.plan();
+  I.dec.plan();
+  I.flags = I.send.flags | I.own.flags;
+  I.blob.upload({&I.send, &I.own, &I.dec});
+  I.recv_stride = align_up(std::max<std::uint64_t>(layout_.chunks[me].msg_bytes, 16), kMsgAlign);
+  I.send_buf.reset(layout_.gather_bytes + 16);
+  I.gather_buf.reset(layout_.gather_bytes + 16);
+  I.recv_buf.reset(I.recv_stride * (N - 1) + 16);
+  I.bad.reset(16);
+  cuda_check(cudaMemset(I.bad.get(), 0xFF, 16), "memset");
+  if (I.flags & GCX_F_NEEDS_ZERO) {
+    cuda_check(cudaMemset(I.send_buf.get(), 0, I.send_buf.size()), "memset");
+    cuda_check(cudaMemset(I.gather_buf.get(), 0, I.gather_buf.size()), "memset");
+  }
+}
+
+DeviceReducer::~DeviceReducer() = default;
+
+void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_seed, ReduceOp op,
+                              void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const std::size_t N = layout_.nodes, me = std::size_t(comm_.rank()), d = layout_.d;
+  if (N == 1) {
+    if (in != out)
+      cuda_check(cudaMemcpyAsync(out, in, 4 * d, cudaMemcpyDeviceToDevice, st), "copy");
+    return;
+  }
+  Impl& I = *impl_;
+  ncclComm_t comm = static_cast<ncclComm_t>(comm_.handle());
+  const float divisor = op == ReduceOp::average ? float(N) : 1.0f;
+  if (I.flags & GCX_F_NEEDS_ZERO) {
+    cuda_check(cudaMemsetAsync(I.send_buf.get(), 0, I.send_buf.size(), st), "memset");
+    cuda_check(cudaMemsetAsync(I.gather_buf.get<std::uint8_t>() + layout_.gather_offset[me], 0,
+                               layout_.chunks[me].msg_bytes, st), "memset");
+  }
+  auto* bad = I.bad.get<unsigned long long>();
+  // K1: my share of every other owner's chunk, seed hop_seed(step, 0, me)
+  gcx_check(gcx_encode_pieces(I.blob.pieces(I.send), I.blob.prefix(I.send),
+                              std::uint32_t(I.send.pieces.size()), I.send.ntiles, I.send.flags,
+                              hop_seed(step_seed, 0, me), in, I.send_buf.get<std::uint8_t>(),
+                              bad, st));
+  // round 1: all-to-all of compressed chunks
+  const std::uint64_t m_me = layout_.chunks[me].msg_bytes;
+  nccl_check(ncclGroupStart(), "ncclGroupStart");
+  for (std::size_t j = 1; j < N; ++j) {
+    const std::size_t peer = (me + j) % N;
+    const std::size_t src = (me + N - j) % N;
+    if (layout_.chunks[peer].msg_bytes)
+      nccl_check(ncclSend(I.send_buf.get<std::uint8_t>() + layout_.gather_offset[peer],
+                          layout_.chunks[peer].msg_bytes, ncclUint8, int(peer), comm, st),
+                 "ncclSend");
+    if (m_me)
+      nccl_check(ncclRecv(I.recv_buf.get<std::uint8_t>() + (src < me ? src : src - 1) * I.recv_stride,
+                          m_me, ncclUint8, int(src), comm, st),
+                 "ncclRecv");
+  }
+  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  // K2: fold (ascending id, own raw) + requantize (hop 1) + own output
+  std::uint8_t* bcast = I.gather_buf.get<std::uint8_t>() + layout_.gather_offset[me];
+  gcx_check(gcx_sra_reduce(I.blob.pieces(I.own), I.blob.prefix(I.own),
+                           std::uint32_t(I.own.pieces.size()), I.own.ntiles, I.own.flags,
+                           I.recv_buf.get<std::uint8_t>(), I.recv_stride, in, std::uint32_t(N),
+                           std::uint32_t(me), hop_seed(step_seed, 1, me), bcast, out, divisor,
+                           bad + 1, st));
+  // round 2: variable-size all-gather of the owners' compressed aggregates
+  nccl_check(ncclGroupStart(), "ncclGroupStart");
+  for (std::size_t j = 1; j < N; ++j) {
+    const std::size_t peer = (me + j) % N;
+    const std::size_t src = (me + N - j) % N;
+    if (m_me) nccl_check(ncclSend(bcast, m_me, ncclUint8, int(peer), comm, st), "ncclSend");
+    if (layout_.chunks[src].msg_bytes)
+      nccl_check(ncclRecv(I.gather_buf.get<std::uint8_t>() + layout_.gather_offset[src],
+                          layout_.chunks[src].msg_bytes, ncclUint8, int(src), comm, st),
+                 "ncclRecv");
+  }
+  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  // K3: decode the other owners' chunks (+ average)
+  gcx_check(gcx_decode_pieces(I.blob.pieces(I.dec), I.blob.prefix(I.dec),
+                              std::uint32_t(I.dec.pieces.size()), I.dec.ntiles,
+                              I.gather_buf.get<std::uint8_t>(), out, divisor, st));
+}
+
+StepTrace DeviceReducer::trace() const {
+  StepTrace t = sra_trace(layout_);
+  if (impl_ && layout_.nodes > 1) {
+    std::uint64_t bad[2];
+    cuda_check(cudaMemcpy(bad, impl_->bad.get(), 16, cudaMemcpyDeviceToHost), "D2H");
+    for (int k = 0; k < 2; ++k)
+      if (bad[k] != ~0ULL) throw_non_finite(k == 0 ? impl_->send : impl_->own, bad[k]);
+  }
+  return t;
+}
+
+std::uint64_t DeviceReducer::device_bytes_sent() const {
+  const std::size_t N = layout_.nodes, me = std::size_t(comm_.rank());
+  std::uint64_t b = 0;
+  for (std::size_t c = 0; c < N; ++c)
+    if (c != me) b += layout_.chunks[c].msg_bytes + layout_.chunks[me].msg_bytes;
+  return b;
+}
+
+int DeviceReducer::launches_per_call() const {
+  if (layout_.nodes <= 1) return 0;
+  int k = 3;
+  if (impl_->flags & GCX_F_BIG_BUCKETS) k += 4;
+  return k;
+}
+
+}  // namespace gcomm::collectives

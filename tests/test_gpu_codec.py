@@ -1,0 +1,115 @@
+"""K1/K3 parity through the C-ABI on the GPU: bit-exact packed codes, norms
+and dequantized values against the oracle."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from tests.golden_inputs import make_input
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2111_08617_b200 import device
+    return device
+
+
+def _gpu_codec(dev, v, bits, bucket, seed):
+    x = torch.from_numpy(v).cuda()
+    norms, packed, bad = dev.quantize(x, bits, bucket, seed)
+    deq = dev.dequantize(norms, packed, v.size, bits, bucket)
+    torch.cuda.synchronize()
+    dev.check_finite(bad)
+    nbytes = (v.size * (bits + 1) + 7) // 8
+    return norms.cpu().numpy(), packed.cpu().numpy()[:nbytes], deq.cpu().numpy()
+
+
+def test_golden_codec_cases_bit_exact(dev, oracle):
+    with open(os.path.join(GOLD, "codec.json")) as f:
+        cases = json.load(f)["cases"]
+    for c in cases:
+        v = make_input(c["n"], c["gen"])
+        if c["n"] == 0:
+            continue
+        norms, packed, deq = _gpu_codec(dev, v, c["bits"], c["bucket"], c["seed"])
+        assert oracle.fnv1a64(norms) == c["norms_fnv"], c
+        assert oracle.fnv1a64(packed) == c["packed_fnv"], c
+        assert oracle.fnv1a64(deq) == c["deq_fnv"], c
+
+
+def test_c1_full_size_digests(dev, oracle):
+    """C1 = 1e-3*normal01(0x5eed, i), n = 25,557,032, 4b/128, seed 42."""
+    n = 25_557_032
+    v = oracle.normal_vector(n, 0x5EED, 1e-3)
+    norms, packed, deq = _gpu_codec(dev, v, 4, 128, 42)
+    assert packed.size == 15_973_145 and norms.size == 199_665
+    assert oracle.fnv1a64(packed) == 0x48061E58E8EFC214
+    assert oracle.fnv1a64(norms) == 0xA0F211F9B3554F9A
+    assert oracle.fnv1a64(deq) == 0x475F012FF75F72F5
+
+
+@pytest.mark.parametrize("bits", range(1, 9))
+@pytest.mark.parametrize("bucket", [1, 5, 64, 128, 512, 1024, 3000, 5000, 10000])
+def test_random_matrix_vs_oracle(dev, oracle, bits, bucket):
+    rng = np.random.default_rng(bits * 7919 + bucket)
+    n = int(rng.integers(1, 60000))
+    v = (rng.standard_normal(n) * 10.0 ** rng.integers(-30, 30)).astype(np.float32)
+    v[rng.random(n) < 0.02] = np.float32(-0.0)
+    v[rng.random(n) < 0.02] = 0.0
+    seed = int(rng.integers(0, 2**63))
+    norms, packed, deq = _gpu_codec(dev, v, bits, bucket, seed)
+    wn, wp = oracle.quantize(v, bits, bucket, seed)
+    assert (norms.view(np.uint32) == wn.view(np.uint32)).all()
+    assert (packed == wp).all()
+    wd = oracle.dequantize(wn, wp, n, bits, bucket)
+    assert (deq.view(np.uint32) == wd.view(np.uint32)).all()
+
+
+def test_error_bound_and_norm_bound(dev, oracle):
+    """proj/tests/codec_test.cpp:78-96 on the GPU output."""
+    n = 1_000_000
+    v = oracle.normal_vector(n, 7)
+    norms, packed, deq = _gpu_codec(dev, v, 3, 128, 99)
+    bound = norms.astype(np.float64)[np.arange(n) // 128] / 7
+    err = np.abs(deq.astype(np.float64) - v)
+    assert (err <= bound * (1 + 1e-5)).all()
+    assert (np.abs(deq) <= bound * 7 * (1 + 1e-5)).all()
+
+
+def test_non_finite_reports_first_index(dev):
+    v = np.ones(1000, np.float32)
+    v[700] = np.inf
+    v[901] = np.nan
+    x = torch.from_numpy(v).cuda()
+    _, _, bad = dev.quantize(x, 4, 128, 0)
+    torch.cuda.synchronize()
+    with pytest.raises(ValueError, match="index 700"):
+        dev.check_finite(bad)
+
+
+def test_dequant_exhaustive_levels(dev, oracle):
+    """Every level of every width against random norms (A6 exactness)."""
+    rng = np.random.default_rng(5)
+    for bits in range(1, 9):
+        s = (1 << bits) - 1
+        nb = 4096
+        norms = np.abs(rng.standard_normal(nb) * 10.0 ** rng.integers(-35, 35, nb)).astype(np.float32)
+        bucket = s + 1
+        n = nb * bucket
+        levels = np.tile(np.arange(s + 1, dtype=np.uint32), nb)
+        signs = (rng.random(n) < 0.5).astype(np.uint8)
+        packed = oracle.pack_levels(levels, signs, bits)
+        want = oracle.dequantize(norms, packed, n, bits, bucket)
+        cap = np.zeros((packed.size + 3) // 4 * 4, np.uint8)
+        cap[: packed.size] = packed
+        got = dev.dequantize(torch.from_numpy(norms).cuda(), torch.from_numpy(cap).cuda(), n,
+                             bits, bucket).cpu().numpy()
+        assert (got.view(np.uint32) == want.view(np.uint32)).all(), bits

@@ -1,0 +1,200 @@
+"""Engine (dense SRA path, static and adaptive plans) and adaptive planner on
+the GPU, against the reference engine (src/engine.cpp) run through SimNet
+via oracle/_ref, or the golden digests it produced (tests/golden/engine.json).
+Plus the properties of /root/reference/proj/tests/engine_test.cpp and
+adaptive_test.cpp."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import RefOracle, engine_inputs
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def g():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2111_08617_b200 import _gcomm
+    return _gcomm
+
+
+KINDS = ["weight", "bias", "norm", "embedding", "other"]
+
+
+def run_engine(g, oracle, nodes, layers, steps, tag, plan_json=None, adaptive_json=None,
+               step_seed=1, fuse_limit=0):
+    cfg = g.EngineConfig()
+    cfg.nodes = nodes
+    cfg.step_seed = step_seed
+    if fuse_limit:
+        cfg.fuse_limit_bytes = fuse_limit
+    if plan_json:
+        cfg.plan = g.CompressionPlan.from_json(plan_json)
+    if adaptive_json:
+        cfg.plan_source = g.PlanSource.adaptive
+        cfg.adaptive = g.AdaptiveConfig.from_json(adaptive_json)
+    eng = g.Engine(cfg)
+    digests = []
+    for k in range(steps):
+        ins = engine_inputs(oracle, layers, nodes, k, tag)
+        for r in range(nodes):
+            for t, (name, n, kind, _) in enumerate(layers):
+                eng.submit(r, g.GradientTensor(g.LayerSpec(name, n, getattr(g.LayerKind, KINDS[kind])),
+                                               ins[r][t]))
+        outs = [eng.flush(r) for r in range(nodes)]
+        blobs = [np.concatenate([t.values for t in o]) for o in outs]
+        for b in blobs[1:]:
+            assert (b.view(np.uint32) == blobs[0].view(np.uint32)).all()
+        digests.append(oracle.fnv1a64(blobs[0]))
+    return digests, eng
+
+
+def engine_cases():
+    with open(os.path.join(GOLD, "engine.json")) as f:
+        return json.load(f)["cases"]
+
+
+@pytest.mark.parametrize("case", engine_cases(), ids=lambda c: c["name"])
+def test_engine_matches_reference(g, oracle, case):
+    layers = [tuple(x) for x in case["layers"]]
+    got, eng = run_engine(g, oracle, case["nodes"], layers, case["steps"], case["tag"],
+                          case.get("plan"), case.get("adaptive"), case.get("step_seed", 1),
+                          case.get("fuse_limit", 0))
+    want = case["digests"]
+    if RefOracle.available():  # recompute with the compiled reference when shipped
+        want, _ = RefOracle().engine_run(case["nodes"], layers, case["steps"], case["tag"],
+                                         case.get("plan"), case.get("adaptive"),
+                                         case.get("step_seed", 1), case.get("fuse_limit", 0))
+        assert want == case["digests"]
+    assert got == want
+    swaps = [json.loads(line) for line in eng.events_json().splitlines()
+             if json.loads(line)["event"] == "plan_swap"]
+    assert [(s["step"], s["payload"]["bits"]) for s in swaps] == \
+        [tuple(x) for x in case.get("plan_swaps", [])]
+
+
+def test_single_node_passthrough(g, oracle):
+    """engine_test.cpp:62-75"""
+    cfg = g.EngineConfig()
+    cfg.nodes = 1
+    eng = g.Engine(cfg)
+    a = oracle.normal_vector(100, 1)
+    b = oracle.normal_vector(9, 2)
+    eng.submit(0, g.GradientTensor(g.LayerSpec("w", 100, g.LayerKind.weight), a))
+    eng.submit(0, g.GradientTensor(g.LayerSpec("b", 9, g.LayerKind.bias), b))
+    out = eng.flush(0)
+    assert (out[0].values == a).all() and (out[1].values == b).all()
+    assert eng.steps_completed() == 1 and eng.last_trace().total_bytes_sent() == 0
+
+
+def test_barrier_misuse_rejected(g, oracle):
+    """engine_test.cpp:175-206"""
+    cfg = g.EngineConfig()
+    cfg.nodes = 2
+    eng = g.Engine(cfg)
+    v = oracle.normal_vector(8192, 3)
+    w = g.LayerSpec("w", 8192, g.LayerKind.weight)
+    eng.submit(0, g.GradientTensor(w, v))
+    with pytest.raises(g.ProtocolError):
+        eng.submit(0, g.GradientTensor(w, v))
+    eng.submit(1, g.GradientTensor(w, v))
+    eng.flush(0)
+    with pytest.raises(g.OrderingError):
+        eng.submit(0, g.GradientTensor(w, v))
+    with pytest.raises(g.OrderingError):
+        eng.flush(0)
+    eng.flush(1)
+    eng.submit(0, g.GradientTensor(g.LayerSpec("w2", 8192, g.LayerKind.weight), v))
+    # layout drift against the first step
+    with pytest.raises(g.ProtocolError):
+        eng.submit(1, g.GradientTensor(g.LayerSpec("other", 5, g.LayerKind.weight), v[:5]))
+
+
+def test_composed_codec_bound(g, oracle):
+    """engine_test.cpp:122-173: quantized averaging inside (2/s) max(max1, max2)."""
+    nodes, d, bucket, s = 8, 4096, 128, 15.0
+    cfg = g.EngineConfig()
+    cfg.nodes = nodes
+    eng = g.Engine(cfg)
+    inputs = [oracle.normal_vector(d, 900 + n) for n in range(nodes)]
+    for n in range(nodes):
+        eng.submit(n, g.GradientTensor(g.LayerSpec("w", d, g.LayerKind.weight), inputs[n]))
+    outs = [eng.flush(n)[0].values for n in range(nodes)]
+    mean = inputs[0].copy()
+    for x in inputs[1:]:
+        mean += x
+    mean /= np.float32(nodes)
+    X = np.stack(inputs).astype(np.float64)
+    max1 = max(np.sqrt((X[n, b * bucket:(b + 1) * bucket] ** 2).sum())
+               for n in range(nodes) for b in range(d // bucket))
+    tot = X.sum(0)
+    max2 = max(np.sqrt((tot[b * bucket:(b + 1) * bucket] ** 2).sum()) +
+               (nodes - 1) * np.sqrt(bucket) * max1 / s for b in range(d // bucket))
+    bound = (2.0 / s) * max(max1, max2)
+    worst = np.abs(outs[0].astype(np.float64) - mean).max()
+    assert 0.0 < worst <= bound
+
+
+def _population(g, oracle, seed):
+    """bench.cpp:197-227 transformer_like_population, fed through the device
+    StatsCollector."""
+    shapes = [("embed.tok", 8 << 20, 0.001), ("layer0.attn.w", 1 << 19, 0.01),
+              ("layer0.mlp.w", 1 << 19, 0.012), ("layer1.attn.w", 1 << 19, 0.01),
+              ("layer1.mlp.w", 1 << 19, 0.012), ("layer2.attn.w", 1 << 19, 0.01),
+              ("layer2.mlp.w", 1 << 19, 0.012), ("layer3.attn.w", 1 << 19, 0.01),
+              ("layer3.mlp.w", 1 << 19, 0.012), ("embed.pos", 1 << 17, 0.3),
+              ("head.w", 1 << 17, 0.35)]
+    col = g.StatsCollector(0.01)
+    for name, n, scale in shapes:
+        key = oracle.hash_combine(seed, g.fnv1a64(name))
+        col.add(name, oracle.normal_vector(n, key, scale))
+    col.finish_step()
+    return col.stats(), col.snapshots()
+
+
+def test_kmeans_plan_on_canned_population(g, oracle):
+    """bench_test.cpp:173-190"""
+    stats, snaps = _population(g, oracle, 1)
+    by = {s.name: s for s in stats}
+    assert abs(by["embed.tok"].l2_norm - 0.001 * 2896.3) < 0.02 * 0.001 * 2896.3
+    assert abs(by["head.w"].l2_norm - 0.35 * 362.0) < 0.02 * 0.35 * 362.0
+    cfg = g.AdaptiveConfig()
+    cfg.method = "kmeans"
+    cfg.palette = [2, 4, 8]
+    cfg.clusters = 3
+    cfg.alpha = 1.0
+    cfg.bucket_size = 128
+    d = g.build_plan(stats, snaps, cfg)
+    assert d.within_budget and d.plan_error <= d.baseline_error
+    assert d.bits["embed.tok"] == 2
+    assert d.bits["layer0.attn.w"] == 4 and d.bits["layer3.mlp.w"] == 4
+    assert d.bits["embed.pos"] == 8 and d.bits["head.w"] == 8
+    assert d.compression_ratio >= 1.2
+
+
+def test_stats_collector_window_sums(g, oracle):
+    """adaptive_test.cpp:52-90: elementwise FP64 window sums, f32 snapshots."""
+    col = g.StatsCollector(0.25)
+    a = oracle.normal_vector(1000, 5)
+    b = oracle.normal_vector(1000, 6)
+    col.add("w", a)
+    col.finish_step()
+    col.add("w", b)
+    col.finish_step()
+    snap = col.snapshots()["w"]
+    want = (a.astype(np.float64) + b.astype(np.float64)).astype(np.float32)
+    assert (snap == want).all()
+    st = col.stats()[0]
+    tot = a.astype(np.float64) + b.astype(np.float64)
+    assert abs(st.l2_norm - np.sqrt((tot ** 2).sum())) <= 1e-12 * st.l2_norm
+    top = np.sort(tot ** 2)[::-1][:250].sum()
+    assert abs(st.top_fraction_norm - np.sqrt(top)) <= 1e-12 * st.top_fraction_norm
+    with pytest.raises(ValueError, match="fed twice"):
+        col.add("w", a)
+        col.add("w", a)
