@@ -228,6 +228,32 @@ PYBIND11_MODULE(_gcomm, m) {
   m.def("hop_seed", &collectives::hop_seed);
   m.def("latency_rounds", &collectives::latency_rounds);
   m.def("chunk_boundaries", &collectives::chunk_boundaries);
+  m.def("sra_layout", [](std::size_t d, std::size_t nodes,
+                         const std::vector<collectives::Segment>& segs) {
+    const auto L = collectives::make_layout(d, nodes, segs);
+    py::dict out;
+    out["bounds"] = L.bounds;
+    out["gather_offset"] = L.gather_offset;
+    out["gather_bytes"] = L.gather_bytes;
+    std::vector<std::uint64_t> msg, wire, q;
+    py::list pieces;
+    for (const auto& ch : L.chunks) {
+      msg.push_back(ch.msg_bytes);
+      wire.push_back(ch.wire_bytes);
+      q.push_back(ch.quantized_pieces);
+      py::list pl;
+      for (const auto& p : ch.pieces)
+        pl.append(py::make_tuple(p.src, p.len, p.norms, p.packed, p.bucket, p.bits));
+      pieces.append(pl);
+    }
+    out["msg_bytes"] = msg;
+    out["wire_bytes"] = wire;
+    out["quantized_pieces"] = q;
+    out["pieces"] = pieces;
+    const auto tr = collectives::sra_trace(L);
+    out["bytes_sent"] = tr.bytes_sent;
+    return out;
+  });
   m.def("allreduce", &collectives::allreduce, py::arg("request"), py::arg("nodes"),
         py::call_guard<py::gil_scoped_release>());
 
@@ -337,8 +363,8 @@ PYBIND11_MODULE(_gcomm, m) {
   });
 
   // ---- engine ----
-  static py::exception<engine::ProtocolError> protocol_error(m, "ProtocolError", PyExc_RuntimeError);
-  static py::exception<engine::OrderingError> ordering_error(m, "OrderingError", PyExc_RuntimeError);
+  py::register_exception<engine::ProtocolError>(m, "ProtocolError", PyExc_RuntimeError);
+  py::register_exception<engine::OrderingError>(m, "OrderingError", PyExc_RuntimeError);
   py::enum_<engine::PlanSource>(m, "PlanSource")
       .value("static_plan", engine::PlanSource::static_plan)
       .value("adaptive", engine::PlanSource::adaptive);

@@ -1,0 +1,135 @@
+"""bench.py's N > 1 leg: compressed SRA allreduce of the ResNet-50 per-layer
+gradient list (BASELINE.json configs[1]) on N B200s, one rank per GPU.
+
+One step = the average of all fused gradient buffers across ranks
+(K1 -> NCCL all-to-all -> K2 -> NCCL all-gather -> K3 per buffer).
+value = effective bus GB/s = (4n / t) * 2(N-1)/N, t = max over ranks.
+Beside it: uncompressed NCCL fp32 allreduce of the same buffers (the
+baseline the north star asks to beat), timed the same way.
+"""
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import time
+
+
+def run(args, metric, ClockSampler, measured_peaks, cpu_codec_sample):
+    import torch
+    import torch.distributed as dist
+
+    from . import _gcomm as G
+    from .ddp import CompressedAllreduce, load_layout, make_communicator
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = make_communicator(rank, world)
+    layers = load_layout("resnet50")
+    car = CompressedAllreduce(layers, comm)
+    n = car.elements
+    g = torch.Generator(device="cuda").manual_seed(0xC2 + rank)
+    stream = torch.cuda.current_stream()
+
+    def fill():
+        for buf in car.flat:
+            buf.normal_(generator=g).mul_(1e-3)
+
+    fill()
+    for k in range(args.warmup):
+        car.allreduce(k)
+    torch.cuda.synchronize()
+    dist.barrier()
+
+    # timed region: refill inputs (outside events) so every step reduces fresh data
+    steps_ms = []
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            fill()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            car.allreduce(args.warmup + k)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            steps_ms.append(e0.elapsed_time(e1))
+    t = torch.tensor([sum(steps_ms) / len(steps_ms)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+
+    # baseline: uncompressed NCCL fp32 allreduce of the same buffers
+    for _ in range(3):
+        for buf in car.flat:
+            dist.all_reduce(buf)
+    torch.cuda.synchronize()
+    b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    b0.record(stream)
+    for _ in range(args.steps):
+        for buf in car.flat:
+            dist.all_reduce(buf)
+    b1.record(stream)
+    torch.cuda.synchronize()
+    tb = torch.tensor([b0.elapsed_time(b1) / args.steps], device="cuda")
+    dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+    base_ms = float(tb.item())
+
+    # end to end with host buffers: pinned H2D of the gradient, reduce, D2H
+    host_in = [torch.empty(b.numel(), dtype=torch.float32, pin_memory=True).normal_()
+               for b in car.flat]
+    host_out = [torch.empty_like(h) for h in host_in]
+    torch.cuda.synchronize()
+    dist.barrier()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record(stream)
+    for k in range(args.steps):
+        for h, buf in zip(host_in, car.flat):
+            buf.copy_(h, non_blocking=True)
+        car.allreduce(10_000 + k)
+        for h, buf in zip(host_out, car.flat):
+            h.copy_(buf, non_blocking=True)
+    x1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([x0.elapsed_time(x1) / args.steps], device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+
+    busbw = lambda ms_: (4 * n / (ms_ * 1e-3)) * 2 * (world - 1) / world / 1e9  # noqa: E731
+    peak, peak_kind = measured_peaks()
+    wire = car.wire_bytes_sent()
+    dev_bytes = car.device_bytes_sent()
+    if rank == 0:
+        line = {
+            "metric": metric, "value": busbw(ms), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 in, f64 codec math, u8 packed", "data": "synthetic (torch.randn * 1e-3)",
+            "config": {"workload": "ResNet-50 per-layer gradient list (161 tensors, 25,557,032 "
+                                   "floats), default filter, 4-bit/128, 64 MiB fused buffers, "
+                                   "SRA average",
+                       "parallelism": f"dp{world}", "buffers": len(car.buffers),
+                       "convention": "busbw = (4n/t)*2(N-1)/N (nccl-tests)",
+                       "nccl_fp32_allreduce_ms": base_ms,
+                       "nccl_fp32_busbw_GBps": busbw(base_ms),
+                       "speedup_vs_nccl_fp32": base_ms / ms,
+                       "wire_bytes_sent_per_rank": wire, "device_bytes_sent_per_rank": dev_bytes,
+                       "nvlink_GBps_on_compressed_bytes": dev_bytes / (ms * 1e-3) / 1e9,
+                       "l2": "inputs refilled before every step (102 MB/rank, rotating RNG)"},
+            "roofline": {"bound": "nvlink", "achieved": dev_bytes / (ms * 1e-3) / 1e9,
+                         "peak": 770.0, "unit": "GB/s",
+                         "frac": dev_bytes / (ms * 1e-3) / 1e9 / 770.0, "traffic": None,
+                         "kernel": "whole SRA step (compressed bytes over NVLink)",
+                         "peak_kind": "measured peer copy per direction (B200_PROFILING.md)"},
+            "cpu_baseline": None,
+            "e2e": {"value": busbw(e2e_ms), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
+                    "d2h_bytes_per_step": 4 * n},
+            "gpu_launches": car.launches_per_step() * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0

@@ -110,8 +110,10 @@ def test_barrier_misuse_rejected(g, oracle):
     with pytest.raises(g.OrderingError):
         eng.flush(0)
     eng.flush(1)
-    eng.submit(0, g.GradientTensor(g.LayerSpec("w2", 8192, g.LayerKind.weight), v))
     # layout drift against the first step
+    with pytest.raises(g.ProtocolError, match="established layout"):
+        eng.submit(0, g.GradientTensor(g.LayerSpec("w2", 8192, g.LayerKind.weight), v))
+    eng.submit(0, g.GradientTensor(w, v))
     with pytest.raises(g.ProtocolError):
         eng.submit(1, g.GradientTensor(g.LayerSpec("other", 5, g.LayerKind.weight), v[:5]))
 
