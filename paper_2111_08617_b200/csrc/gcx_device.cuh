@@ -80,6 +80,49 @@ __device__ __forceinline__ void mix64_split(uint32_t& lo, uint32_t& hi, const Op
   xorshift(lo, hi, 31, o.m31);
 }
 
+// Variant "ALU shifts, 3-IMAD multiplies": z *= C as mul.wide + two chained
+// mad.lo (3 FMA-pipe ops, no separate add), all shifts on the ALU pipe.
+__device__ __forceinline__ void mul64c_mad(uint32_t& lo, uint32_t& hi, uint32_t cl, uint32_t ch) {
+  unsigned long long w;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(w) : "r"(lo), "r"(cl));
+  uint32_t t, nhi;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(lo), "r"(ch), "r"(uint32_t(w >> 32)));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(nhi) : "r"(hi), "r"(cl), "r"(t));
+  lo = uint32_t(w);
+  hi = nhi;
+}
+
+__device__ __forceinline__ void xorshift_alu(uint32_t& lo, uint32_t& hi, uint32_t k) {
+  const uint32_t f = __funnelshift_r(lo, hi, k);
+  const uint32_t t = hi >> k;
+  lo ^= f;
+  hi ^= t;
+}
+
+__device__ __forceinline__ void mix64_alu(uint32_t& lo, uint32_t& hi) {
+  asm("add.cc.u32 %0, %0, 0x7f4a7c15;\n\taddc.u32 %1, %1, 0x9e3779b9;" : "+r"(lo), "+r"(hi));
+  xorshift_alu(lo, hi, 30);
+  mul64c_mad(lo, hi, 0x1ce4e5b9u, 0xbf58476du);
+  xorshift_alu(lo, hi, 27);
+  mul64c_mad(lo, hi, 0x133111ebu, 0x94d049bbu);
+  xorshift_alu(lo, hi, 31);
+}
+
+__device__ __forceinline__ void draw_key_alu(uint32_t i_lo, uint32_t i_hi, uint32_t b_lo,
+                                             uint32_t b_hi, uint32_t s_lo, uint32_t s_hi,
+                                             uint32_t& h_lo, uint32_t& h_hi) {
+  uint32_t lo = i_lo, hi = i_hi;
+  mix64_alu(lo, hi);
+  lo ^= b_lo;
+  hi ^= b_hi;
+  mix64_alu(lo, hi);
+  lo ^= s_lo;
+  hi ^= s_hi;
+  mix64_alu(lo, hi);
+  h_lo = lo;
+  h_hi = hi;
+}
+
 // h = mix64(seed ^ mix64(b ^ mix64(i)))  (uniform01's key, util.hpp:26-29)
 __device__ __forceinline__ void draw_key(uint32_t i_lo, uint32_t i_hi, uint32_t b_lo, uint32_t b_hi,
                                          uint32_t s_lo, uint32_t s_hi, const Opq& o,
