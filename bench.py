@@ -235,7 +235,7 @@ def run_codec(args):
     achieved = q_bytes / (q_ms * 1e-3) / 1e9
     cb = cpu_codec_sample(reps=3)
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "round1_k1_quantize_pipe.json")
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("bytes_per_launch")

@@ -57,6 +57,16 @@ typedef struct gcx_piece {
   int32_t bits;    /* 1..8 magnitude bits; 0 = raw f32 (CodecMode::uncompressed) */
 } gcx_piece;
 
+/* Key-sharing work item: pieces order[first .. first+npieces) all cover the
+ * piece-local index range [i0, i0 + count) (clipped to each piece's length)
+ * and, under one seed, draw identical uniform01 keys there. */
+typedef struct gcx_work {
+  uint32_t i0;
+  uint32_t count;
+  uint32_t first;
+  uint32_t npieces;
+} gcx_work;
+
 int gcx_version(void);
 const char* gcx_last_error(void);
 
@@ -88,6 +98,18 @@ int gcx_dequantize(const float* norms, const uint8_t* packed, uint64_t n, int bi
  *         divisor != 1 (IEEE f32 division, finalize() average). */
 int gcx_encode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
                       uint32_t ntiles, uint32_t flags, uint64_t seed, const float* src,
+                      uint8_t* msg, unsigned long long* bad_key, void* stream);
+/* Key-sharing encode plan for a piece table quantized under ONE seed (SRA
+ * stage 1: every piece of a sender's hop, collectives.cpp:252-253): group
+ * pieces by bucket size, and let each work item draw the keys of an index
+ * range once for up to 16 pieces.  Fills work[] (capacity work_cap) and
+ * order[npieces]; returns the number of work items, 0 if the table is not
+ * eligible (a bucket > 2048), or <0 on error. */
+int64_t gcx_plan_shared(const gcx_piece* pieces, uint32_t npieces, gcx_work* work,
+                        uint32_t work_cap, uint32_t* order, uint32_t* flags);
+/* Same result as gcx_encode_pieces (bit-identical), from a gcx_plan_shared plan. */
+int gcx_encode_shared(const gcx_piece* pieces, const gcx_work* work, const uint32_t* order,
+                      uint32_t nwork, uint32_t flags, uint64_t seed, const float* src,
                       uint8_t* msg, unsigned long long* bad_key, void* stream);
 int gcx_decode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
                       uint32_t ntiles, const uint8_t* msg, float* dst, float divisor,

@@ -58,6 +58,8 @@ _decl("gcx_quantize", i32, vp, u64, i32, u64, u64, vp, vp, vp, vp)
 _decl("gcx_dequantize", i32, vp, vp, u64, i32, u64, vp, vp)
 _decl("gcx_encode_pieces", i32, vp, vp, u32, u32, u32, u64, vp, vp, vp, vp)
 _decl("gcx_decode_pieces", i32, vp, vp, u32, u32, vp, vp, C.c_float, vp)
+_decl("gcx_plan_shared", i64, C.POINTER(Piece), u32, vp, u32, C.POINTER(u32), C.POINTER(u32))
+_decl("gcx_encode_shared", i32, vp, vp, vp, u32, u32, u64, vp, vp, vp, vp)
 _decl("gcx_sra_reduce", i32, vp, vp, u32, u32, u32, vp, u64, vp, u32, u32, u64, vp, vp,
       C.c_float, vp, vp)
 _decl("gcx_hash_bench", i32, u64, u64, u32, i32, vp, vp)
@@ -66,7 +68,8 @@ _decl("gcx_device_info", i32, i32, C.POINTER(i32), C.POINTER(i32))
 EXPORTS = ["gcx_version", "gcx_last_error", "gcx_compressed_size", "gcx_packed_bytes",
            "gcx_packed_capacity", "gcx_hop_seed", "gcx_uniform01", "gcx_plan_tiles",
            "gcx_quantize", "gcx_dequantize", "gcx_encode_pieces", "gcx_decode_pieces",
-           "gcx_sra_reduce", "gcx_hash_bench", "gcx_device_info"]
+           "gcx_sra_reduce", "gcx_hash_bench", "gcx_device_info", "gcx_plan_shared",
+           "gcx_encode_shared"]
 
 
 def lib():

@@ -241,13 +241,33 @@ struct Table {
   std::uint32_t flags = 0;
   std::size_t dev_off = 0;  // byte offset of the pieces in the blob
   std::size_t pre_off = 0;
-  void plan() {
+  // key-sharing encode plan (one seed for the whole table: SRA stage 1)
+  std::vector<gcx_work> work;
+  std::vector<std::uint32_t> order;
+  std::uint32_t shared_flags = 0;
+  std::size_t work_off = 0, order_off = 0;
+  void plan(bool want_shared = false) {
     prefix.assign(pieces.size() + 1, 0);
     const std::int64_t nt =
         gcx_plan_tiles(pieces.data(), std::uint32_t(pieces.size()), prefix.data(), &flags);
     if (nt < 0) gcx_check(int(nt));
     ntiles = std::uint32_t(nt);
+    work.clear();
+    order.clear();
+    if (want_shared && !pieces.empty()) {
+      std::uint64_t cap = 16;
+      for (const auto& p : pieces) cap += p.len / 512 + 2;
+      work.resize(cap);
+      order.resize(pieces.size());
+      const std::int64_t nw = gcx_plan_shared(pieces.data(), std::uint32_t(pieces.size()),
+                                              work.data(), std::uint32_t(cap), order.data(),
+                                              &shared_flags);
+      if (nw < 0) gcx_check(int(nw));
+      work.resize(std::size_t(nw));
+      if (nw == 0) order.clear();
+    }
   }
+  bool shared() const { return !work.empty(); }
 };
 
 struct TableBlob {
@@ -259,12 +279,20 @@ struct TableBlob {
       off = align_up(off + sizeof(gcx_piece) * std::max<std::size_t>(1, t->pieces.size()), 16);
       t->pre_off = off;
       off = align_up(off + 4 * t->prefix.size(), 16);
+      t->work_off = off;
+      off = align_up(off + sizeof(gcx_work) * t->work.size(), 16);
+      t->order_off = off;
+      off = align_up(off + 4 * t->order.size() + 4, 16);
     }
     std::vector<std::uint8_t> host(off, 0);
     for (Table* t : tables) {
       if (!t->pieces.empty())
         std::memcpy(host.data() + t->dev_off, t->pieces.data(), sizeof(gcx_piece) * t->pieces.size());
       std::memcpy(host.data() + t->pre_off, t->prefix.data(), 4 * t->prefix.size());
+      if (!t->work.empty())
+        std::memcpy(host.data() + t->work_off, t->work.data(), sizeof(gcx_work) * t->work.size());
+      if (!t->order.empty())
+        std::memcpy(host.data() + t->order_off, t->order.data(), 4 * t->order.size());
     }
     buf.reset(off);
     cuda_check(cudaMemcpy(buf.get(), host.data(), off, cudaMemcpyHostToDevice), "table upload");
@@ -275,7 +303,24 @@ struct TableBlob {
   const std::uint32_t* prefix(const Table& t) const {
     return reinterpret_cast<const std::uint32_t*>(buf.get<std::uint8_t>() + t.pre_off);
   }
+  const gcx_work* work(const Table& t) const {
+    return reinterpret_cast<const gcx_work*>(buf.get<std::uint8_t>() + t.work_off);
+  }
+  const std::uint32_t* order(const Table& t) const {
+    return reinterpret_cast<const std::uint32_t*>(buf.get<std::uint8_t>() + t.order_off);
+  }
 };
+
+// K1 over a sender's table: the key-sharing kernel when the plan allows it
+void encode(const TableBlob& blob, const Table& t, std::uint64_t seed, const float* src,
+            std::uint8_t* msg, unsigned long long* bad, cudaStream_t st) {
+  if (t.shared())
+    gcx_check(gcx_encode_shared(blob.pieces(t), blob.work(t), blob.order(t),
+                                std::uint32_t(t.work.size()), t.shared_flags, seed, src, msg, bad, st));
+  else
+    gcx_check(gcx_encode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
+                                t.ntiles, t.flags, seed, src, msg, bad, st));
+}
 
 Table shifted(const std::vector<gcx_piece>& src, std::uint64_t delta) {
   Table t;
@@ -342,10 +387,10 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
       append(dec[id], L.chunks[c].pieces, L.gather_offset[c]);
     }
     own[id] = shifted(L.chunks[id].pieces, 0);
-    send[id].plan();
+    send[id].plan(true);
     own[id].plan();
     dec[id].plan();
-    flags |= send[id].flags | own[id].flags;
+    flags |= send[id].flags | send[id].shared_flags | own[id].flags;
   }
   std::vector<Table*> all;
   for (std::size_t k = 0; k < N; ++k) {
@@ -376,10 +421,8 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
   const float divisor = req.op == ReduceOp::average ? float(N) : 1.0f;
   // stage 1 (scatter): every sender encodes its share of every other chunk
   for (std::size_t id = 0; id < N; ++id)
-    gcx_check(gcx_encode_pieces(blob.pieces(send[id]), blob.prefix(send[id]),
-                                std::uint32_t(send[id].pieces.size()), send[id].ntiles,
-                                send[id].flags, hop_seed(req.step_seed, 0, id),
-                                in.get<float>() + id * d, mail.get<std::uint8_t>(), badp + id, st));
+    encode(blob, send[id], hop_seed(req.step_seed, 0, id), in.get<float>() + id * d,
+           mail.get<std::uint8_t>(), badp + id, st);
   // owners: ascending-id fold, hop-1 re-encode, decode own bytes
   for (std::size_t c = 0; c < N; ++c)
     gcx_check(gcx_sra_reduce(blob.pieces(own[c]), blob.prefix(own[c]),
@@ -480,10 +523,10 @@ DeviceReducer::DeviceReducer(Communicator& comm, std::size_t d, std::vector<Segm
     append(I.dec, layout_.chunks[c].pieces, layout_.gather_offset[c]);
   }
   I.own = shifted(layout_.chunks[me].pieces, 0);
-  I.send.plan();
+  I.send.plan(true);
   I.own.plan();
   I.dec.plan();
-  I.flags = I.send.flags | I.own.flags;
+  I.flags = I.send.flags | I.send.shared_flags | I.own.flags;
   I.blob.upload({&I.send, &I.own, &I.dec});
   I.recv_stride = align_up(std::max<std::uint64_t>(layout_.chunks[me].msg_bytes, 16), kMsgAlign);
   I.send_buf.reset(layout_.gather_bytes + 16);
@@ -518,10 +561,7 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
   }
   auto* bad = I.bad.get<unsigned long long>();
   // K1: my share of every other owner's chunk, seed hop_seed(step, 0, me)
-  gcx_check(gcx_encode_pieces(I.blob.pieces(I.send), I.blob.prefix(I.send),
-                              std::uint32_t(I.send.pieces.size()), I.send.ntiles, I.send.flags,
-                              hop_seed(step_seed, 0, me), in, I.send_buf.get<std::uint8_t>(),
-                              bad, st));
+  encode(I.blob, I.send, hop_seed(step_seed, 0, me), in, I.send_buf.get<std::uint8_t>(), bad, st);
   // round 1: all-to-all of compressed chunks
   const std::uint64_t m_me = layout_.chunks[me].msg_bytes;
   nccl_check(ncclGroupStart(), "ncclGroupStart");

@@ -113,3 +113,68 @@ def test_dequant_exhaustive_levels(dev, oracle):
         got = dev.dequantize(torch.from_numpy(norms).cuda(), torch.from_numpy(cap).cuda(), n,
                              bits, bucket).cpu().numpy()
         assert (got.view(np.uint32) == want.view(np.uint32)).all(), bits
+
+
+def test_shared_key_encode_matches_plain(dev, oracle):
+    """gcx_encode_shared (keys drawn once per index range for all pieces of a
+    bucket size, collectives.cpp:252-253's one-seed-per-hop) must equal
+    gcx_encode_pieces byte for byte, and both the oracle per piece."""
+    import ctypes as C
+    from paper_2111_08617_b200 import _capi
+    rng = np.random.default_rng(17)
+    lens = [int(x) for x in rng.integers(1, 9000, 23)] + [8192, 8191, 1, 4096]
+    pieces, off, src_off = [], 0, 0
+    for k, n in enumerate(lens):
+        bits = int(rng.integers(1, 9)) if k % 5 else 0
+        bucket = int(rng.choice([7, 64, 128, 512, 2048])) if bits else 0
+        nb = (n + bucket - 1) // bucket if bits else 0
+        if bits:
+            norms_off = off
+            packed_off = (off + 4 * nb + 15) // 16 * 16
+            off = (packed_off + _capi.packed_capacity(n, bits) + 15) // 16 * 16
+        else:
+            norms_off = packed_off = off
+            off = (off + 4 * n + 15) // 16 * 16
+        pieces.append(_capi.Piece(src_off, n, norms_off, packed_off, 0, bucket, bits))
+        src_off += n
+    x = (rng.standard_normal(src_off) * 10.0 ** rng.integers(-3, 3)).astype(np.float32)
+    xd = torch.from_numpy(x).cuda()
+    seed = 0xABCDEF12345
+    nt, prefix, flags = _capi.plan_tiles(pieces)
+    arr = (_capi.Piece * len(pieces))(*pieces)
+    cap = 4096
+    work = (C.c_uint32 * (4 * cap))()
+    order = (C.c_uint32 * len(pieces))()
+    sflags = C.c_uint32(0)
+    nw = _capi.lib().gcx_plan_shared(arr, len(pieces), C.cast(work, C.c_void_p), cap, order,
+                                     C.byref(sflags))
+    assert nw > 0
+    dev_pieces = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).cuda()
+    dev_prefix = torch.tensor(prefix, dtype=torch.int32).cuda()
+    dev_work = torch.tensor(list(work)[: 4 * nw], dtype=torch.int32).cuda()
+    dev_order = torch.tensor(list(order), dtype=torch.int32).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for shared in (False, True):
+        msg = torch.zeros(off + 64, dtype=torch.uint8, device="cuda")
+        bad = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+        if shared:
+            rc = _capi.lib().gcx_encode_shared(dev_pieces.data_ptr(), dev_work.data_ptr(),
+                                               dev_order.data_ptr(), nw, sflags.value, seed,
+                                               xd.data_ptr(), msg.data_ptr(), bad.data_ptr(), st)
+        else:
+            rc = _capi.lib().gcx_encode_pieces(dev_pieces.data_ptr(), dev_prefix.data_ptr(),
+                                               len(pieces), nt, flags, seed, xd.data_ptr(),
+                                               msg.data_ptr(), bad.data_ptr(), st)
+        _capi.check(rc)
+        torch.cuda.synchronize()
+        outs.append(msg.cpu().numpy())
+    assert (outs[0] == outs[1]).all()
+    for p in pieces:
+        if p.bits == 0:
+            continue
+        wn, wp = oracle.quantize(x[p.src:p.src + p.len], p.bits, p.bucket, seed)
+        nb = wn.size
+        got_n = outs[1][p.norms:p.norms + 4 * nb].view(np.float32)
+        assert (got_n.view(np.uint32) == wn.view(np.uint32)).all()
+        assert (outs[1][p.packed:p.packed + wp.size] == wp).all()
