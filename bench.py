@@ -197,7 +197,7 @@ def run_codec(args):
     # form, 1 = pipe-balanced split form used by K1/K2, 2 = split form 2-way ILP
     sink = torch.zeros(1, dtype=torch.int64, device="cuda")
     hash_ms = {}
-    for variant in (0, 1, 2, 3, 4):
+    for variant in (0, 1, 2, 3, 4, 5, 6):
         dev.hash_bench(n, 42, bucket, sink, variant)
         torch.cuda.synchronize()
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -123,6 +123,51 @@ __device__ __forceinline__ void draw_key_alu(uint32_t i_lo, uint32_t i_hi, uint3
   h_hi = hi;
 }
 
+// Variant "opaque shifts": the shift amounts live in registers ptxas cannot
+// constant-fold, so every 64-bit right shift stays a funnel SHF (half rate on
+// B200) instead of being rewritten as IMAD.HI by a power of two (quarter rate
+// on B200; scripts/piperate.cu measures both).
+struct Shk {
+  uint32_t k30, k27, k31;
+};
+
+__device__ __forceinline__ Shk make_shk() {
+  Shk k{30u, 27u, 31u};
+  asm volatile("" : "+r"(k.k30), "+r"(k.k27), "+r"(k.k31));
+  return k;
+}
+
+__device__ __forceinline__ void xorshift_shf(uint32_t& lo, uint32_t& hi, uint32_t k) {
+  const uint32_t f = __funnelshift_r(lo, hi, k);
+  const uint32_t t = __funnelshift_r(hi, 0u, k);
+  lo ^= f;
+  hi ^= t;
+}
+
+__device__ __forceinline__ void mix64_shf(uint32_t& lo, uint32_t& hi, const Shk& k) {
+  asm("add.cc.u32 %0, %0, 0x7f4a7c15;\n\taddc.u32 %1, %1, 0x9e3779b9;" : "+r"(lo), "+r"(hi));
+  xorshift_shf(lo, hi, k.k30);
+  mul64c(lo, hi, 0x1ce4e5b9u, 0xbf58476du);
+  xorshift_shf(lo, hi, k.k27);
+  mul64c(lo, hi, 0x133111ebu, 0x94d049bbu);
+  xorshift_shf(lo, hi, k.k31);
+}
+
+__device__ __forceinline__ void draw_key_shf(uint32_t i_lo, uint32_t i_hi, uint32_t b_lo,
+                                             uint32_t b_hi, uint32_t s_lo, uint32_t s_hi,
+                                             const Shk& k, uint32_t& h_lo, uint32_t& h_hi) {
+  uint32_t lo = i_lo, hi = i_hi;
+  mix64_shf(lo, hi, k);
+  lo ^= b_lo;
+  hi ^= b_hi;
+  mix64_shf(lo, hi, k);
+  lo ^= s_lo;
+  hi ^= s_hi;
+  mix64_shf(lo, hi, k);
+  h_lo = lo;
+  h_hi = hi;
+}
+
 // h = mix64(seed ^ mix64(b ^ mix64(i)))  (uniform01's key, util.hpp:26-29)
 __device__ __forceinline__ void draw_key(uint32_t i_lo, uint32_t i_hi, uint32_t b_lo, uint32_t b_hi,
                                          uint32_t s_lo, uint32_t s_hi, const Opq& o,
