@@ -1,8 +1,20 @@
 #!/bin/bash
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q -x --timeout=240 --timeout-method=thread > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 120 ./scripts/piperate > gpurun_out/piperate.log 2>&1
-timeout 300 python scripts/variant_bench.py > gpurun_out/variants.log 2>&1
 timeout 300 python scripts/sra_emul_bench.py > gpurun_out/sra_emul.log 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/sra_launches.csv python scripts/sra_emul_profile.py 8 > gpurun_out/sra_prof.log 2>&1
 timeout 200 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
-tail -4 gpurun_out/pytest_gpu.log; cat gpurun_out/variants.log gpurun_out/sra_emul.log; python -c "import json; d=json.load(open('gpurun_out/bench.json')); print(d['config']['hash_only_ms'], d['config']['quantize_ms'], d['config']['dequantize_ms'])"
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 > /dev/null 2>&1
+tail -4 gpurun_out/pytest_gpu.log; cat gpurun_out/sra_emul.log; python -c "import json; d=json.load(open('gpurun_out/bench.json')); print(d['value'], d['config']['hash_only_ms'], d['config']['quantize_ms'], d['config']['dequantize_ms'])"
+python - <<'PY'
+import csv, collections
+rows=list(csv.reader(open("gpurun_out/sra_launches.csv")))
+for i,r in enumerate(rows):
+    if r and r[0]=="ID": hdr=r; start=i; break
+data=[dict(zip(hdr,r)) for r in rows[start+1:] if len(r)==len(hdr)]
+half=data[len(data)//2:]
+agg=collections.defaultdict(lambda:[0,0.0])
+for d in half:
+    k=d["Kernel Name"].split("(")[0][-40:]; agg[k][0]+=1; agg[k][1]+=float(d["Metric Value"])
+for k,(c,t) in sorted(agg.items(), key=lambda x:-x[1][1]): print(f"{k:40s} {c:3d} {t/1e3:9.1f} us")
+PY

@@ -12,8 +12,9 @@
  *   gcx_compressed_size codec::compressed_size_bytes src/codec.cpp:151-156
  *   gcx_encode_pieces   encode_pieces (quantize+serialize per piece)  src/collectives.cpp:143-163
  *   gcx_decode_pieces   decode_pieces (+ finalize's average)          src/collectives.cpp:165-194, :213-228
- *   gcx_sra_reduce      run_sra owner step: ascending-id fold, hop-1
- *                       re-encode, owner decodes its own bytes       src/collectives.cpp:258-292
+ *   gcx_fold_pieces     run_sra owner fold (ascending id, own raw)   src/collectives.cpp:258-279
+ *   gcx_sra_reduce      run_sra owner step: fold, hop-1 re-encode,
+ *                       owner decodes its own bytes                  src/collectives.cpp:258-292
  *   gcx_hop_seed        collectives::hop_seed  src/collectives.cpp:29-31
  *   gcx_uniform01       uniform01              include/gcomm/util.hpp:26-29
  *
@@ -55,17 +56,18 @@ typedef struct gcx_piece {
   uint64_t seed;   /* per-piece seed (only with GCX_F_PIECE_SEEDS) */
   uint32_t bucket; /* bucket size (quantized pieces) */
   int32_t bits;    /* 1..8 magnitude bits; 0 = raw f32 (CodecMode::uncompressed) */
+  uint64_t keys;   /* element offset of this piece's run in a key table
+                      (gcx_plan_keys), or UINT64_MAX: draw keys inline */
 } gcx_piece;
 
-/* Key-sharing work item: pieces order[first .. first+npieces) all cover the
- * piece-local index range [i0, i0 + count) (clipped to each piece's length)
- * and, under one seed, draw identical uniform01 keys there. */
-typedef struct gcx_work {
-  uint32_t i0;
-  uint32_t count;
-  uint32_t first;
-  uint32_t npieces;
-} gcx_work;
+/* One run of a key table: keys[off + i] = the uniform01 key of piece-local
+ * index i (< len) for bucket size `bucket` (util.hpp:26-29 before the >> 11). */
+typedef struct gcx_keygroup {
+  uint64_t off;
+  uint64_t len;
+  uint32_t bucket;
+  uint32_t pad;
+} gcx_keygroup;
 
 int gcx_version(void);
 const char* gcx_last_error(void);
@@ -93,39 +95,44 @@ int gcx_dequantize(const float* norms, const uint8_t* packed, uint64_t n, int bi
 
 /* ---- piece-table codec (device tables; tile_prefix from gcx_plan_tiles) ----
  * encode: src + pieces[k].src ... -> msg + pieces[k].norms/packed.  Raw pieces
- *         are copied.  bad_key = (piece << 40) | piece-local index.
+ *         are copied.  bad_key = (piece << 40) | piece-local index.  keys: a
+ *         key table made by gcx_make_keys for this seed (or NULL: inline).
  * decode: msg -> dst + pieces[k].src, each value divided by `divisor` when
  *         divisor != 1 (IEEE f32 division, finalize() average). */
 int gcx_encode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
                       uint32_t ntiles, uint32_t flags, uint64_t seed, const float* src,
-                      uint8_t* msg, unsigned long long* bad_key, void* stream);
-/* Key-sharing encode plan for a piece table quantized under ONE seed (SRA
- * stage 1: every piece of a sender's hop, collectives.cpp:252-253): group
- * pieces by bucket size, and let each work item draw the keys of an index
- * range once for up to 16 pieces.  Fills work[] (capacity work_cap) and
- * order[npieces]; returns the number of work items, 0 if the table is not
- * eligible (a bucket > 2048), or <0 on error. */
-int64_t gcx_plan_shared(const gcx_piece* pieces, uint32_t npieces, gcx_work* work,
-                        uint32_t work_cap, uint32_t* order, uint32_t* flags);
-/* Same result as gcx_encode_pieces (bit-identical), from a gcx_plan_shared plan. */
-int gcx_encode_shared(const gcx_piece* pieces, const gcx_work* work, const uint32_t* order,
-                      uint32_t nwork, uint32_t flags, uint64_t seed, const float* src,
-                      uint8_t* msg, unsigned long long* bad_key, void* stream);
+                      uint8_t* msg, const unsigned long long* keys,
+                      unsigned long long* bad_key, void* stream);
+/* Key tables for a piece table quantized under ONE seed (SRA stage 1 uses
+ * one seed for every piece of a sender's hop, collectives.cpp:252-253; the
+ * owner's re-encode one seed for its whole chunk): pieces of one bucket size
+ * draw the same key at the same piece-local index (codec.cpp:60), so one run
+ * per bucket size, as long as its longest piece, serves them all.
+ * plan_keys sets pieces[k].keys, fills groups[], returns the table length. */
+int64_t gcx_plan_keys(gcx_piece* pieces, uint32_t npieces, gcx_keygroup* groups,
+                      uint32_t group_cap, uint32_t* ngroups);
+int gcx_make_keys(const gcx_keygroup* groups, uint32_t ngroups, uint64_t total, uint64_t seed,
+                  unsigned long long* keys, void* stream);
 int gcx_decode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
                       uint32_t ntiles, const uint8_t* msg, float* dst, float divisor,
                       void* stream);
 
-/* ---- SRA owner step (fused dequantize-accumulate-requantize) ----
- * Pieces are chunk-local (src = offset inside the owner's chunk).  The
- * contribution of node id is `own` when id == me, else the message in recv
- * slot (id < me ? id : id-1) at recv + slot*slot_stride.  Folds ascending id
- * in f32, re-encodes with `seed` into bcast, and writes the owner's decoded
- * result (divided by divisor) to out. */
+/* ---- SRA owner step ----
+ * fold: the contribution of node id is `own` when id == me, else the message
+ * in recv slot (id < me ? id : id-1) at recv + slot*slot_stride; folds
+ * ascending id in f32 (collectives.cpp:268-279) and writes the aggregate to
+ * out + pieces[k].src (pieces are the owner's chunk, src = buffer offsets).
+ * sra_reduce: fold, re-encode the aggregate with `seed` into bcast, and write
+ * the owner's decoded result (divided by divisor) to out
+ * (collectives.cpp:283-292). */
+int gcx_fold_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
+                    uint32_t ntiles, const uint8_t* recv, uint64_t slot_stride, const float* own,
+                    uint32_t nodes, uint32_t me, float* out, void* stream);
 int gcx_sra_reduce(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
                    uint32_t ntiles, uint32_t flags, const uint8_t* recv, uint64_t slot_stride,
                    const float* own, uint32_t nodes, uint32_t me, uint64_t seed,
-                   uint8_t* bcast, float* out, float divisor, unsigned long long* bad_key,
-                   void* stream);
+                   uint8_t* bcast, float* out, float divisor, const unsigned long long* keys,
+                   unsigned long long* bad_key, void* stream);
 
 /* ---- microbenchmarks ----
  * Integer ceiling of the reference RNG: n draws of uniform01(seed, i/bucket, i),

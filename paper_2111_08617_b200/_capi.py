@@ -23,14 +23,27 @@ class GcxError(RuntimeError):
     pass
 
 
+NO_KEYS = 0xFFFFFFFFFFFFFFFF
+
+
 class Piece(C.Structure):
     """gcx_piece (include/gcx.h)."""
     _fields_ = [("src", C.c_uint64), ("len", C.c_uint64), ("norms", C.c_uint64),
                 ("packed", C.c_uint64), ("seed", C.c_uint64), ("bucket", C.c_uint32),
-                ("bits", C.c_int32)]
+                ("bits", C.c_int32), ("keys", C.c_uint64)]
+
+    def __init__(self, src=0, len=0, norms=0, packed=0, seed=0, bucket=0, bits=0,
+                 keys=NO_KEYS):
+        super().__init__(src, len, norms, packed, seed, bucket, bits, keys)
 
 
-assert C.sizeof(Piece) == 48
+class KeyGroup(C.Structure):
+    """gcx_keygroup (include/gcx.h)."""
+    _fields_ = [("off", C.c_uint64), ("len", C.c_uint64), ("bucket", C.c_uint32),
+                ("pad", C.c_uint32)]
+
+
+assert C.sizeof(Piece) == 56 and C.sizeof(KeyGroup) == 24
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")
@@ -56,20 +69,21 @@ _decl("gcx_uniform01", C.c_double, u64, u64, u64)
 _decl("gcx_plan_tiles", i64, C.POINTER(Piece), u32, C.POINTER(u32), C.POINTER(u32))
 _decl("gcx_quantize", i32, vp, u64, i32, u64, u64, vp, vp, vp, vp)
 _decl("gcx_dequantize", i32, vp, vp, u64, i32, u64, vp, vp)
-_decl("gcx_encode_pieces", i32, vp, vp, u32, u32, u32, u64, vp, vp, vp, vp)
+_decl("gcx_encode_pieces", i32, vp, vp, u32, u32, u32, u64, vp, vp, vp, vp, vp)
 _decl("gcx_decode_pieces", i32, vp, vp, u32, u32, vp, vp, C.c_float, vp)
-_decl("gcx_plan_shared", i64, C.POINTER(Piece), u32, vp, u32, C.POINTER(u32), C.POINTER(u32))
-_decl("gcx_encode_shared", i32, vp, vp, vp, u32, u32, u64, vp, vp, vp, vp)
+_decl("gcx_plan_keys", i64, C.POINTER(Piece), u32, C.POINTER(KeyGroup), u32, C.POINTER(u32))
+_decl("gcx_make_keys", i32, vp, u32, u64, u64, vp, vp)
+_decl("gcx_fold_pieces", i32, vp, vp, u32, u32, vp, u64, vp, u32, u32, vp, vp)
 _decl("gcx_sra_reduce", i32, vp, vp, u32, u32, u32, vp, u64, vp, u32, u32, u64, vp, vp,
-      C.c_float, vp, vp)
+      C.c_float, vp, vp, vp)
 _decl("gcx_hash_bench", i32, u64, u64, u32, i32, vp, vp)
 _decl("gcx_device_info", i32, i32, C.POINTER(i32), C.POINTER(i32))
 
 EXPORTS = ["gcx_version", "gcx_last_error", "gcx_compressed_size", "gcx_packed_bytes",
            "gcx_packed_capacity", "gcx_hop_seed", "gcx_uniform01", "gcx_plan_tiles",
            "gcx_quantize", "gcx_dequantize", "gcx_encode_pieces", "gcx_decode_pieces",
-           "gcx_sra_reduce", "gcx_hash_bench", "gcx_device_info", "gcx_plan_shared",
-           "gcx_encode_shared"]
+           "gcx_sra_reduce", "gcx_hash_bench", "gcx_device_info", "gcx_plan_keys",
+           "gcx_make_keys", "gcx_fold_pieces"]
 
 
 def lib():

@@ -233,41 +233,37 @@ StepTrace sra_trace(const SraLayout& L) {
 
 namespace {
 
-// A device piece table with its tile prefix, uploaded into one blob.
+// A device piece table with its tile prefix (and, for tables quantized under
+// one seed, its key-table plan), uploaded into one blob.
 struct Table {
   std::vector<gcx_piece> pieces;
   std::vector<std::uint32_t> prefix;
   std::uint32_t ntiles = 0;
   std::uint32_t flags = 0;
-  std::size_t dev_off = 0;  // byte offset of the pieces in the blob
+  std::size_t dev_off = 0;  // byte offsets in the blob
   std::size_t pre_off = 0;
-  // key-sharing encode plan (one seed for the whole table: SRA stage 1)
-  std::vector<gcx_work> work;
-  std::vector<std::uint32_t> order;
-  std::uint32_t shared_flags = 0;
-  std::size_t work_off = 0, order_off = 0;
-  void plan(bool want_shared = false) {
+  std::vector<gcx_keygroup> groups;
+  std::uint64_t key_len = 0;  // key-table entries this table needs
+  std::size_t grp_off = 0;
+  void plan(bool with_keys = false) {
     prefix.assign(pieces.size() + 1, 0);
     const std::int64_t nt =
         gcx_plan_tiles(pieces.data(), std::uint32_t(pieces.size()), prefix.data(), &flags);
     if (nt < 0) gcx_check(int(nt));
     ntiles = std::uint32_t(nt);
-    work.clear();
-    order.clear();
-    if (want_shared && !pieces.empty()) {
-      std::uint64_t cap = 16;
-      for (const auto& p : pieces) cap += p.len / 512 + 2;
-      work.resize(cap);
-      order.resize(pieces.size());
-      const std::int64_t nw = gcx_plan_shared(pieces.data(), std::uint32_t(pieces.size()),
-                                              work.data(), std::uint32_t(cap), order.data(),
-                                              &shared_flags);
-      if (nw < 0) gcx_check(int(nw));
-      work.resize(std::size_t(nw));
-      if (nw == 0) order.clear();
+    groups.clear();
+    key_len = 0;
+    for (auto& p : pieces) p.keys = ~0ULL;
+    if (with_keys && !pieces.empty()) {
+      groups.resize(pieces.size());
+      std::uint32_t ng = 0;
+      const std::int64_t len = gcx_plan_keys(pieces.data(), std::uint32_t(pieces.size()),
+                                             groups.data(), std::uint32_t(groups.size()), &ng);
+      if (len < 0) gcx_check(int(len));
+      groups.resize(ng);
+      key_len = std::uint64_t(len);
     }
   }
-  bool shared() const { return !work.empty(); }
 };
 
 struct TableBlob {
@@ -279,20 +275,17 @@ struct TableBlob {
       off = align_up(off + sizeof(gcx_piece) * std::max<std::size_t>(1, t->pieces.size()), 16);
       t->pre_off = off;
       off = align_up(off + 4 * t->prefix.size(), 16);
-      t->work_off = off;
-      off = align_up(off + sizeof(gcx_work) * t->work.size(), 16);
-      t->order_off = off;
-      off = align_up(off + 4 * t->order.size() + 4, 16);
+      t->grp_off = off;
+      off = align_up(off + sizeof(gcx_keygroup) * t->groups.size() + 16, 16);
     }
     std::vector<std::uint8_t> host(off, 0);
     for (Table* t : tables) {
       if (!t->pieces.empty())
         std::memcpy(host.data() + t->dev_off, t->pieces.data(), sizeof(gcx_piece) * t->pieces.size());
       std::memcpy(host.data() + t->pre_off, t->prefix.data(), 4 * t->prefix.size());
-      if (!t->work.empty())
-        std::memcpy(host.data() + t->work_off, t->work.data(), sizeof(gcx_work) * t->work.size());
-      if (!t->order.empty())
-        std::memcpy(host.data() + t->order_off, t->order.data(), 4 * t->order.size());
+      if (!t->groups.empty())
+        std::memcpy(host.data() + t->grp_off, t->groups.data(),
+                    sizeof(gcx_keygroup) * t->groups.size());
     }
     buf.reset(off);
     cuda_check(cudaMemcpy(buf.get(), host.data(), off, cudaMemcpyHostToDevice), "table upload");
@@ -303,23 +296,23 @@ struct TableBlob {
   const std::uint32_t* prefix(const Table& t) const {
     return reinterpret_cast<const std::uint32_t*>(buf.get<std::uint8_t>() + t.pre_off);
   }
-  const gcx_work* work(const Table& t) const {
-    return reinterpret_cast<const gcx_work*>(buf.get<std::uint8_t>() + t.work_off);
-  }
-  const std::uint32_t* order(const Table& t) const {
-    return reinterpret_cast<const std::uint32_t*>(buf.get<std::uint8_t>() + t.order_off);
+  const gcx_keygroup* groups(const Table& t) const {
+    return reinterpret_cast<const gcx_keygroup*>(buf.get<std::uint8_t>() + t.grp_off);
   }
 };
 
-// K1 over a sender's table: the key-sharing kernel when the plan allows it
+// K1 over a table quantized under one seed: draw the shared key runs once
+// (gcx_make_keys), then norms + quantize + pack reading keys from the table
 void encode(const TableBlob& blob, const Table& t, std::uint64_t seed, const float* src,
-            std::uint8_t* msg, unsigned long long* bad, cudaStream_t st) {
-  if (t.shared())
-    gcx_check(gcx_encode_shared(blob.pieces(t), blob.work(t), blob.order(t),
-                                std::uint32_t(t.work.size()), t.shared_flags, seed, src, msg, bad, st));
-  else
-    gcx_check(gcx_encode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
-                                t.ntiles, t.flags, seed, src, msg, bad, st));
+            std::uint8_t* msg, unsigned long long* keys, unsigned long long* bad,
+            cudaStream_t st) {
+  const bool use_keys = keys != nullptr && t.key_len > 0;
+  if (use_keys)
+    gcx_check(gcx_make_keys(blob.groups(t), std::uint32_t(t.groups.size()), t.key_len, seed, keys,
+                            st));
+  gcx_check(gcx_encode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
+                              t.ntiles, t.flags, seed, src, msg, use_keys ? keys : nullptr, bad,
+                              st));
 }
 
 Table shifted(const std::vector<gcx_piece>& src, std::uint64_t delta) {
@@ -379,18 +372,21 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
   }
   std::vector<Table> send(N), own(N), dec(N);
   std::uint32_t flags = 0;
+  std::uint64_t key_len = 0;
   for (std::size_t id = 0; id < N; ++id) {
     for (std::size_t c = 0; c < N; ++c) {
-      if (c == id) continue;
-      const std::uint64_t slot = id < c ? id : id - 1;
-      append(send[id], L.chunks[c].pieces, mbase[c] + slot * slot_stride[c]);
-      append(dec[id], L.chunks[c].pieces, L.gather_offset[c]);
+      if (c != id) {
+        const std::uint64_t slot = id < c ? id : id - 1;
+        append(send[id], L.chunks[c].pieces, mbase[c] + slot * slot_stride[c]);
+      }
+      append(dec[id], L.chunks[c].pieces, L.gather_offset[c]);  // own chunk too
     }
     own[id] = shifted(L.chunks[id].pieces, 0);
     send[id].plan(true);
-    own[id].plan();
+    own[id].plan(true);
     dec[id].plan();
-    flags |= send[id].flags | send[id].shared_flags | own[id].flags;
+    flags |= send[id].flags | own[id].flags;
+    key_len = std::max({key_len, send[id].key_len, own[id].key_len});
   }
   std::vector<Table*> all;
   for (std::size_t k = 0; k < N; ++k) {
@@ -404,7 +400,7 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
   detail::Stream stream;
   cudaStream_t st = stream.get();
   DeviceBuffer in(4 * d * N + 16), out(4 * d * N + 16), mail(arena + 16),
-      gather(L.gather_bytes + 16), bad(16 * N);
+      gather(L.gather_bytes + 16), bad(16 * N), keys(8 * key_len + 16);
   for (std::size_t k = 0; k < N; ++k)
     cuda_check(cudaMemcpyAsync(in.get<float>() + k * d, req.inputs[k].data(), 4 * d,
                                cudaMemcpyHostToDevice, st), "H2D");
@@ -418,21 +414,23 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
   cuda_check(cudaEventCreate(&e1), "event");
   cudaEventRecord(e0, st);
   auto* badp = bad.get<unsigned long long>();
+  auto* kp = keys.get<unsigned long long>();
   const float divisor = req.op == ReduceOp::average ? float(N) : 1.0f;
   // stage 1 (scatter): every sender encodes its share of every other chunk
   for (std::size_t id = 0; id < N; ++id)
     encode(blob, send[id], hop_seed(req.step_seed, 0, id), in.get<float>() + id * d,
-           mail.get<std::uint8_t>(), badp + id, st);
-  // owners: ascending-id fold, hop-1 re-encode, decode own bytes
-  for (std::size_t c = 0; c < N; ++c)
-    gcx_check(gcx_sra_reduce(blob.pieces(own[c]), blob.prefix(own[c]),
-                             std::uint32_t(own[c].pieces.size()), own[c].ntiles, own[c].flags,
-                             mail.get<std::uint8_t>() + mbase[c], slot_stride[c],
-                             in.get<float>() + c * d, std::uint32_t(N), std::uint32_t(c),
-                             hop_seed(req.step_seed, 1, c),
-                             gather.get<std::uint8_t>() + L.gather_offset[c],
-                             out.get<float>() + c * d, divisor, badp + N + c, st));
-  // stage 2 (all-gather): everyone decodes the other owners' bytes
+           mail.get<std::uint8_t>(), kp, badp + id, st);
+  // owners: ascending-id fold into out, re-encode with the hop-1 seed
+  for (std::size_t c = 0; c < N; ++c) {
+    gcx_check(gcx_fold_pieces(blob.pieces(own[c]), blob.prefix(own[c]),
+                              std::uint32_t(own[c].pieces.size()), own[c].ntiles,
+                              mail.get<std::uint8_t>() + mbase[c], slot_stride[c],
+                              in.get<float>() + c * d, std::uint32_t(N), std::uint32_t(c),
+                              out.get<float>() + c * d, st));
+    encode(blob, own[c], hop_seed(req.step_seed, 1, c), out.get<float>() + c * d,
+           gather.get<std::uint8_t>() + L.gather_offset[c], kp, badp + N + c, st);
+  }
+  // stage 2 (all-gather): everyone decodes every owner's bytes (own included)
   for (std::size_t id = 0; id < N; ++id)
     gcx_check(gcx_decode_pieces(blob.pieces(dec[id]), blob.prefix(dec[id]),
                                 std::uint32_t(dec[id].pieces.size()), dec[id].ntiles,
@@ -484,7 +482,7 @@ Communicator::~Communicator() {
 struct DeviceReducer::Impl {
   Table send, own, dec;
   TableBlob blob;
-  DeviceBuffer send_buf, recv_buf, gather_buf, bad;
+  DeviceBuffer send_buf, recv_buf, gather_buf, bad, keys;
   std::uint64_t recv_stride = 0;
   std::uint32_t flags = 0;
 };
@@ -518,16 +516,16 @@ DeviceReducer::DeviceReducer(Communicator& comm, std::size_t d, std::vector<Segm
   if (N == 1) return;
   Impl& I = *impl_;
   for (std::size_t c = 0; c < N; ++c) {
-    if (c == me) continue;
-    append(I.send, layout_.chunks[c].pieces, layout_.gather_offset[c]);
-    append(I.dec, layout_.chunks[c].pieces, layout_.gather_offset[c]);
+    if (c != me) append(I.send, layout_.chunks[c].pieces, layout_.gather_offset[c]);
+    append(I.dec, layout_.chunks[c].pieces, layout_.gather_offset[c]);  // own chunk too
   }
   I.own = shifted(layout_.chunks[me].pieces, 0);
   I.send.plan(true);
-  I.own.plan();
+  I.own.plan(true);
   I.dec.plan();
-  I.flags = I.send.flags | I.send.shared_flags | I.own.flags;
+  I.flags = I.send.flags | I.own.flags;
   I.blob.upload({&I.send, &I.own, &I.dec});
+  I.keys.reset(8 * std::max(I.send.key_len, I.own.key_len) + 16);
   I.recv_stride = align_up(std::max<std::uint64_t>(layout_.chunks[me].msg_bytes, 16), kMsgAlign);
   I.send_buf.reset(layout_.gather_bytes + 16);
   I.gather_buf.reset(layout_.gather_bytes + 16);
@@ -560,8 +558,10 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
                                layout_.chunks[me].msg_bytes, st), "memset");
   }
   auto* bad = I.bad.get<unsigned long long>();
+  auto* keys = I.keys.get<unsigned long long>();
   // K1: my share of every other owner's chunk, seed hop_seed(step, 0, me)
-  encode(I.blob, I.send, hop_seed(step_seed, 0, me), in, I.send_buf.get<std::uint8_t>(), bad, st);
+  encode(I.blob, I.send, hop_seed(step_seed, 0, me), in, I.send_buf.get<std::uint8_t>(), keys,
+         bad, st);
   // round 1: all-to-all of compressed chunks
   const std::uint64_t m_me = layout_.chunks[me].msg_bytes;
   nccl_check(ncclGroupStart(), "ncclGroupStart");
@@ -578,13 +578,13 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
                  "ncclRecv");
   }
   nccl_check(ncclGroupEnd(), "ncclGroupEnd");
-  // K2: fold (ascending id, own raw) + requantize (hop 1) + own output
+  // K2: ascending-id fold into out, then re-encode with the hop-1 seed
   std::uint8_t* bcast = I.gather_buf.get<std::uint8_t>() + layout_.gather_offset[me];
-  gcx_check(gcx_sra_reduce(I.blob.pieces(I.own), I.blob.prefix(I.own),
-                           std::uint32_t(I.own.pieces.size()), I.own.ntiles, I.own.flags,
-                           I.recv_buf.get<std::uint8_t>(), I.recv_stride, in, std::uint32_t(N),
-                           std::uint32_t(me), hop_seed(step_seed, 1, me), bcast, out, divisor,
-                           bad + 1, st));
+  gcx_check(gcx_fold_pieces(I.blob.pieces(I.own), I.blob.prefix(I.own),
+                            std::uint32_t(I.own.pieces.size()), I.own.ntiles,
+                            I.recv_buf.get<std::uint8_t>(), I.recv_stride, in, std::uint32_t(N),
+                            std::uint32_t(me), out, st));
+  encode(I.blob, I.own, hop_seed(step_seed, 1, me), out, bcast, keys, bad + 1, st);
   // round 2: variable-size all-gather of the owners' compressed aggregates
   nccl_check(ncclGroupStart(), "ncclGroupStart");
   for (std::size_t j = 1; j < N; ++j) {
@@ -597,7 +597,7 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
                  "ncclRecv");
   }
   nccl_check(ncclGroupEnd(), "ncclGroupEnd");
-  // K3: decode the other owners' chunks (+ average)
+  // K3: decode every owner's chunk (own included) (+ average)
   gcx_check(gcx_decode_pieces(I.blob.pieces(I.dec), I.blob.prefix(I.dec),
                               std::uint32_t(I.dec.pieces.size()), I.dec.ntiles,
                               I.gather_buf.get<std::uint8_t>(), out, divisor, st));
@@ -624,8 +624,9 @@ std::uint64_t DeviceReducer::device_bytes_sent() const {
 
 int DeviceReducer::launches_per_call() const {
   if (layout_.nodes <= 1) return 0;
-  int k = 3;
-  if (impl_->flags & GCX_F_BIG_BUCKETS) k += 4;
+  // make_keys + norms + quant (stage 1), fold + make_keys + norms + quant, decode
+  int k = 8;
+  if (impl_->flags & GCX_F_BIG_BUCKETS) k += 2;
   return k;
 }
 

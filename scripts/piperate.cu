@@ -37,6 +37,17 @@ __global__ void k(uint32_t* out, uint32_t seed) {
         asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(w2) : "r"(a4), "r"(c)); asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(w3) : "r"(a6), "r"(c));
         a0 = uint32_t(w0 >> 32) ^ a1; a2 = uint32_t(w1 >> 32) ^ a3; a4 = uint32_t(w2 >> 32) ^ a5; a6 = uint32_t(w3 >> 32) ^ a7;
         a1 = uint32_t(w0); a3 = uint32_t(w1); a5 = uint32_t(w2); a7 = uint32_t(w3);
+      } else if (OP == 6) {  // LEA.HI: b + (a >> 30) via lea.hi-friendly pattern
+        a0 = (a1 >> 30) + a0; a1 = (a2 >> 30) + a1; a2 = (a3 >> 30) + a2; a3 = (a4 >> 30) + a3;
+        a4 = (a5 >> 30) + a4; a5 = (a6 >> 30) + a5; a6 = (a7 >> 30) + a6; a7 = (a0 >> 30) + a7;
+      } else if (OP == 7) {  // LEA: (a << 5) + b
+        a0 = (a1 << 5) + a0; a1 = (a2 << 5) + a1; a2 = (a3 << 5) + a2; a3 = (a4 << 5) + a3;
+        a4 = (a5 << 5) + a4; a5 = (a6 << 5) + a5; a6 = (a7 << 5) + a6; a7 = (a0 << 5) + a7;
+      } else if (OP == 8) {  // DFMA throughput
+        double d0 = a0, d1 = a1;
+        asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(d0) : "d"(d1));
+        asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(d1) : "d"(d0));
+        a0 = uint32_t(__double_as_longlong(d0)); a1 = uint32_t(__double_as_longlong(d1));
       } else if (OP == 5) {  // IADD3 carry chain pairs (64-bit adds)
         asm volatile("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(a0), "+r"(a1) : "r"(a2), "r"(a3));
         asm volatile("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(a2), "+r"(a3) : "r"(a4), "r"(a5));
@@ -66,5 +77,6 @@ int main() {
   uint32_t* out; cudaMalloc(&out, sms * 8 * 256 * 4);
   run<0>("LOP3", sms, out, 32); run<1>("SHF", sms, out, 32); run<2>("IMAD", sms, out, 32);
   run<3>("IMAD.HI", sms, out, 32); run<4>("IMAD.WIDE", sms, out, 16 + 16); run<5>("IADD3x2", sms, out, 32);
+  run<6>("LEA.HI?", sms, out, 32); run<7>("LEA?", sms, out, 32);
   return 0;
 }

@@ -115,10 +115,11 @@ def test_dequant_exhaustive_levels(dev, oracle):
         assert (got.view(np.uint32) == want.view(np.uint32)).all(), bits
 
 
-def test_shared_key_encode_matches_plain(dev, oracle):
-    """gcx_encode_shared (keys drawn once per index range for all pieces of a
-    bucket size, collectives.cpp:252-253's one-seed-per-hop) must equal
-    gcx_encode_pieces byte for byte, and both the oracle per piece."""
+def test_key_table_encode_matches_inline(dev, oracle):
+    """Pieces quantized under one seed share uniform01 keys per piece-local
+    index and bucket size (codec.cpp:60; collectives.cpp:252-253 uses one seed
+    per sender hop).  Encoding with a gcx_make_keys table must equal inline
+    hashing byte for byte, and both the oracle per piece."""
     import ctypes as C
     from paper_2111_08617_b200 import _capi
     rng = np.random.default_rng(17)
@@ -126,7 +127,7 @@ def test_shared_key_encode_matches_plain(dev, oracle):
     pieces, off, src_off = [], 0, 0
     for k, n in enumerate(lens):
         bits = int(rng.integers(1, 9)) if k % 5 else 0
-        bucket = int(rng.choice([7, 64, 128, 512, 2048])) if bits else 0
+        bucket = int(rng.choice([7, 64, 128, 512, 2048, 5000])) if bits else 0
         nb = (n + bucket - 1) // bucket if bits else 0
         if bits:
             norms_off = off
@@ -140,41 +141,37 @@ def test_shared_key_encode_matches_plain(dev, oracle):
     x = (rng.standard_normal(src_off) * 10.0 ** rng.integers(-3, 3)).astype(np.float32)
     xd = torch.from_numpy(x).cuda()
     seed = 0xABCDEF12345
-    nt, prefix, flags = _capi.plan_tiles(pieces)
     arr = (_capi.Piece * len(pieces))(*pieces)
-    cap = 4096
-    work = (C.c_uint32 * (4 * cap))()
-    order = (C.c_uint32 * len(pieces))()
-    sflags = C.c_uint32(0)
-    nw = _capi.lib().gcx_plan_shared(arr, len(pieces), C.cast(work, C.c_void_p), cap, order,
-                                     C.byref(sflags))
-    assert nw > 0
+    groups = (_capi.KeyGroup * len(pieces))()
+    ng = C.c_uint32(0)
+    total = _capi.lib().gcx_plan_keys(arr, len(pieces), groups, len(pieces), C.byref(ng))
+    assert total > 0 and ng.value >= 5
+    nt, prefix, flags = _capi.plan_tiles(list(arr))
     dev_pieces = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).cuda()
+    dev_groups = torch.frombuffer(bytearray(bytes(groups)), dtype=torch.uint8).cuda()
     dev_prefix = torch.tensor(prefix, dtype=torch.int32).cuda()
-    dev_work = torch.tensor(list(work)[: 4 * nw], dtype=torch.int32).cuda()
-    dev_order = torch.tensor(list(order), dtype=torch.int32).cuda()
+    keys = torch.empty(total, dtype=torch.int64, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
+    _capi.check(_capi.lib().gcx_make_keys(dev_groups.data_ptr(), ng.value, total, seed,
+                                          keys.data_ptr(), st))
     outs = []
-    for shared in (False, True):
+    for use_keys in (False, True):
         msg = torch.zeros(off + 64, dtype=torch.uint8, device="cuda")
         bad = torch.full((1,), -1, dtype=torch.int64, device="cuda")
-        if shared:
-            rc = _capi.lib().gcx_encode_shared(dev_pieces.data_ptr(), dev_work.data_ptr(),
-                                               dev_order.data_ptr(), nw, sflags.value, seed,
-                                               xd.data_ptr(), msg.data_ptr(), bad.data_ptr(), st)
-        else:
-            rc = _capi.lib().gcx_encode_pieces(dev_pieces.data_ptr(), dev_prefix.data_ptr(),
-                                               len(pieces), nt, flags, seed, xd.data_ptr(),
-                                               msg.data_ptr(), bad.data_ptr(), st)
-        _capi.check(rc)
+        _capi.check(_capi.lib().gcx_encode_pieces(
+            dev_pieces.data_ptr(), dev_prefix.data_ptr(), len(pieces), nt, flags, seed,
+            xd.data_ptr(), msg.data_ptr(), keys.data_ptr() if use_keys else None,
+            bad.data_ptr(), st))
         torch.cuda.synchronize()
+        assert int(bad.item()) == -1
         outs.append(msg.cpu().numpy())
     assert (outs[0] == outs[1]).all()
     for p in pieces:
         if p.bits == 0:
+            assert (outs[1][p.norms:p.norms + 4 * p.len].view(np.float32) ==
+                    x[p.src:p.src + p.len]).all()
             continue
         wn, wp = oracle.quantize(x[p.src:p.src + p.len], p.bits, p.bucket, seed)
-        nb = wn.size
-        got_n = outs[1][p.norms:p.norms + 4 * nb].view(np.float32)
+        got_n = outs[1][p.norms:p.norms + 4 * wn.size].view(np.float32)
         assert (got_n.view(np.uint32) == wn.view(np.uint32)).all()
         assert (outs[1][p.packed:p.packed + wp.size] == wp).all()
