@@ -42,6 +42,9 @@ def quantize(x: torch.Tensor, bits: int, bucket: int, seed: int, norms=None, pac
         norms, packed = alloc_compressed(n, bits, bucket, x.device)
     if bad is None:
         bad = torch.full((1,), -1, dtype=torch.int64, device=x.device)
+    elif stream is not None:
+        with torch.cuda.stream(stream):
+            bad.fill_(-1)
     else:
         bad.fill_(-1)
     check(_capi.lib().gcx_quantize(x.data_ptr(), n, bits, bucket, seed & _U64_MAX,
