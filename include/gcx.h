@@ -44,6 +44,8 @@ extern "C" {
 #define GCX_F_BIG_BUCKETS 1u   /* some piece has bucket > GCX_TILE: norm pre-pass */
 #define GCX_F_NEEDS_ZERO 2u    /* some piece's tiles share packed words: zero first */
 #define GCX_F_PIECE_SEEDS 4u   /* use gcx_piece.seed instead of the launch seed */
+#define GCX_F_ODD_BUCKETS 8u   /* some quantized piece has bucket % 32 != 0: generic K1b */
+#define GCX_F_NORM_PASS 16u    /* some piece's norms come from the K1a pre-pass (bucket not 32/64/128) */
 
 #define GCX_TILE 4096          /* max elements per CTA tile */
 
@@ -98,7 +100,8 @@ int gcx_dequantize(const float* norms, const uint8_t* packed, uint64_t n, int bi
  *         are copied.  bad_key = (piece << 40) | piece-local index.  keys: a
  *         key table made by gcx_make_keys for this seed (or NULL: inline).
  * decode: msg -> dst + pieces[k].src, each value divided by `divisor` when
- *         divisor != 1 (IEEE f32 division, finalize() average). */
+ *         divisor != 1 (IEEE f32 division, finalize() average).  flags from
+ *         gcx_plan_tiles (GCX_F_ODD_BUCKETS selects the generic kernel too). */
 int gcx_encode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
                       uint32_t ntiles, uint32_t flags, uint64_t seed, const float* src,
                       uint8_t* msg, const unsigned long long* keys,
@@ -114,8 +117,8 @@ int64_t gcx_plan_keys(gcx_piece* pieces, uint32_t npieces, gcx_keygroup* groups,
 int gcx_make_keys(const gcx_keygroup* groups, uint32_t ngroups, uint64_t total, uint64_t seed,
                   unsigned long long* keys, void* stream);
 int gcx_decode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
-                      uint32_t ntiles, const uint8_t* msg, float* dst, float divisor,
-                      void* stream);
+                      uint32_t ntiles, uint32_t flags, const uint8_t* msg, float* dst,
+                      float divisor, void* stream);
 
 /* ---- SRA owner step ----
  * fold: the contribution of node id is `own` when id == me, else the message

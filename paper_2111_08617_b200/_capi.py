@@ -16,6 +16,8 @@ LIB_PATH = os.path.join(HERE, "libgcx.so")
 GCX_F_BIG_BUCKETS = 1
 GCX_F_NEEDS_ZERO = 2
 GCX_F_PIECE_SEEDS = 4
+GCX_F_ODD_BUCKETS = 8
+GCX_F_NORM_PASS = 16
 GCX_TILE = 4096
 
 
@@ -70,7 +72,7 @@ _decl("gcx_plan_tiles", i64, C.POINTER(Piece), u32, C.POINTER(u32), C.POINTER(u3
 _decl("gcx_quantize", i32, vp, u64, i32, u64, u64, vp, vp, vp, vp)
 _decl("gcx_dequantize", i32, vp, vp, u64, i32, u64, vp, vp)
 _decl("gcx_encode_pieces", i32, vp, vp, u32, u32, u32, u64, vp, vp, vp, vp, vp)
-_decl("gcx_decode_pieces", i32, vp, vp, u32, u32, vp, vp, C.c_float, vp)
+_decl("gcx_decode_pieces", i32, vp, vp, u32, u32, u32, vp, vp, C.c_float, vp)
 _decl("gcx_plan_keys", i64, C.POINTER(Piece), u32, C.POINTER(KeyGroup), u32, C.POINTER(u32))
 _decl("gcx_make_keys", i32, vp, u32, u64, u64, vp, vp)
 _decl("gcx_fold_pieces", i32, vp, vp, u32, u32, vp, u64, vp, u32, u32, vp, vp)

@@ -20,6 +20,15 @@ __device__ __forceinline__ double f32abs_to_f64(uint32_t u_abs) {
   return d;
 }
 
+// Same, branch-free (zero/subnormal via (2^52 + m) - 2^52 = m, times 2^-149),
+// for dependency chains where a branch would sit on the critical path.
+__device__ __forceinline__ double f32abs_to_f64_nb(uint32_t u_abs) {
+  const double dn = __hiloint2double(int((u_abs >> 3) + 0x38000000u), int(u_abs << 29));
+  const double ds = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000, int(u_abs)), 4503599627370496.0),
+                              0x1p-149);
+  return u_abs < 0x00800000u ? ds : dn;
+}
+
 // RN-even double -> float for a non-negative finite q below 2^128; results
 // below the normal float range take the slow conversion.
 __device__ __forceinline__ float f64pos_to_f32_rn(double q) {
@@ -182,6 +191,103 @@ __device__ __forceinline__ void draw_key(uint32_t i_lo, uint32_t i_hi, uint32_t 
   mix64_split(lo, hi, o);
   h_lo = lo;
   h_hi = hi;
+}
+
+// Top word of the uniform01 key only: the final `z ^= z >> 31` of the outer
+// mix64 is applied to the high word alone (the low word is needed only when
+// the 32-bit comparison in quantize_field32 is ambiguous, and that path
+// recomputes the whole key).  HV selects where the high-word right shifts
+// issue: 0 = funnel SHF with opaque amounts (ALU pipe), 1 = plain shifts
+// (ptxas's choice), 2 = IMAD.HI by an opaque power of two (FMA pipe).
+#ifndef GCX_HASH_HV
+#define GCX_HASH_HV 0
+#endif
+template <int HV>
+__device__ __forceinline__ uint32_t shr_hi(uint32_t hi, uint32_t k, uint32_t mk) {
+  if (HV == 0) return __funnelshift_r(hi, 0u, k);
+  if (HV == 1) return hi >> k;
+  return __umulhi(hi, mk);
+}
+
+struct HashK {
+  uint32_t k30, k27, k31, m30, m27, m31;
+};
+
+__device__ __forceinline__ HashK make_hashk() {
+  HashK h{30u, 27u, 31u, 4u, 32u, 2u};
+  asm volatile("" : "+r"(h.k30), "+r"(h.k27), "+r"(h.k31), "+r"(h.m30), "+r"(h.m27), "+r"(h.m31));
+  return h;
+}
+
+template <int HV>
+__device__ __forceinline__ void xorshift_v(uint32_t& lo, uint32_t& hi, uint32_t k, uint32_t mk) {
+  const uint32_t f = __funnelshift_r(lo, hi, k);
+  const uint32_t t = shr_hi<HV>(hi, k, mk);
+  lo ^= f;
+  hi ^= t;
+}
+
+template <int HV>
+__device__ __forceinline__ void mix64_v(uint32_t& lo, uint32_t& hi, const HashK& k) {
+  asm("add.cc.u32 %0, %0, 0x7f4a7c15;\n\taddc.u32 %1, %1, 0x9e3779b9;" : "+r"(lo), "+r"(hi));
+  xorshift_v<HV>(lo, hi, HV == 1 ? 30u : k.k30, k.m30);
+  mul64c(lo, hi, 0x1ce4e5b9u, 0xbf58476du);
+  xorshift_v<HV>(lo, hi, HV == 1 ? 27u : k.k27, k.m27);
+  mul64c(lo, hi, 0x133111ebu, 0x94d049bbu);
+  xorshift_v<HV>(lo, hi, HV == 1 ? 31u : k.k31, k.m31);
+}
+
+template <int HV = GCX_HASH_HV>
+__device__ __forceinline__ uint32_t draw_key_hi(uint32_t i, uint32_t b, uint32_t s_lo,
+                                                uint32_t s_hi, const HashK& k) {
+  uint32_t lo = i, hi = 0u;
+  mix64_v<HV>(lo, hi, k);
+  lo ^= b;
+  mix64_v<HV>(lo, hi, k);
+  lo ^= s_lo;
+  hi ^= s_hi;
+  asm("add.cc.u32 %0, %0, 0x7f4a7c15;\n\taddc.u32 %1, %1, 0x9e3779b9;" : "+r"(lo), "+r"(hi));
+  xorshift_v<HV>(lo, hi, HV == 1 ? 30u : k.k30, k.m30);
+  mul64c(lo, hi, 0x1ce4e5b9u, 0xbf58476du);
+  xorshift_v<HV>(lo, hi, HV == 1 ? 27u : k.k27, k.m27);
+  // hi word of z * 0x94d049bb133111eb, then hi ^= hi >> 31
+  const uint32_t h = __umulhi(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
+  return h ^ shr_hi<HV>(h, HV == 1 ? 31u : k.k31, k.m31);
+}
+
+// |v| (normal, non-zero float bits) as an exact double: exponent rebias only.
+__device__ __forceinline__ double f32normal_to_f64(uint32_t u_abs) {
+  return __hiloint2double(int((u_abs >> 3) + 0x38000000u), int(u_abs << 29));
+}
+
+// ---------------------------------------------------------------------------
+// Fast exact form of one element of codec::quantize (codec.cpp:50-64) for
+// normal non-zero |v| (the caller checks and falls back otherwise):
+//   a  = RN(|v|/norm)       (q0/r/a correction as in quantize_field)
+//   X  = RN(a * s * 2^32)   = RN(a*s) * 2^32 exactly (power-of-two scaling)
+//   T  = RZ(X + 2^52)       = 2^52 + floor(X): x < 2^20, so the low word of T
+//                              is fl = floor(frac(x) * 2^32) and the high
+//                              word's low 20 bits are level = trunc(x)
+//   uniform01 < p  <=>  k53 < frac(x)*2^53 with k53 = h >> 11; decided by the
+//   top key word alone unless hh == fl: hh < fl -> up, hh > fl -> not up.
+// `mn` accumulates min(hh ^ fl): zero flags an ambiguous element, which the
+// caller recomputes with the full key.  Returns level' | sign << BITS.
+// ---------------------------------------------------------------------------
+template <uint32_t BITS>
+__device__ __forceinline__ uint32_t quantize_field32(uint32_t u, double av, double nd, double y,
+                                                     uint32_t hh, uint32_t& mn) {
+  constexpr uint32_t S = (1u << BITS) - 1;
+  constexpr double S2 = double(S) * 4294967296.0;
+  const double q0 = __dmul_rn(av, y);
+  const double r = __fma_rn(-nd, q0, av);
+  const double a = __fma_rn(r, y, q0);
+  const double X = __dmul_rn(a, S2);
+  const double T = __dadd_rz(X, 4503599627370496.0);
+  const uint32_t fl = uint32_t(__double2loint(T));
+  const uint32_t lv = uint32_t(__double2hiint(T)) & 0xFFFFFu;
+  mn = min(mn, hh ^ fl);
+  const uint32_t l = min(lv + (hh < fl ? 1u : 0u), S);
+  return l | ((u >> 31) << BITS);
 }
 
 // reference form, for the microbenchmark and as documentation

@@ -434,7 +434,8 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
   for (std::size_t id = 0; id < N; ++id)
     gcx_check(gcx_decode_pieces(blob.pieces(dec[id]), blob.prefix(dec[id]),
                                 std::uint32_t(dec[id].pieces.size()), dec[id].ntiles,
-                                gather.get<std::uint8_t>(), out.get<float>() + id * d, divisor, st));
+                                dec[id].flags, gather.get<std::uint8_t>(),
+                                out.get<float>() + id * d, divisor, st));
   cudaEventRecord(e1, st);
   result.outputs.assign(N, std::vector<float>(d));
   for (std::size_t k = 0; k < N; ++k)
@@ -599,7 +600,7 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
   nccl_check(ncclGroupEnd(), "ncclGroupEnd");
   // K3: decode every owner's chunk (own included) (+ average)
   gcx_check(gcx_decode_pieces(I.blob.pieces(I.dec), I.blob.prefix(I.dec),
-                              std::uint32_t(I.dec.pieces.size()), I.dec.ntiles,
+                              std::uint32_t(I.dec.pieces.size()), I.dec.ntiles, I.dec.flags,
                               I.gather_buf.get<std::uint8_t>(), out, divisor, st));
 }
 
@@ -624,10 +625,13 @@ std::uint64_t DeviceReducer::device_bytes_sent() const {
 
 int DeviceReducer::launches_per_call() const {
   if (layout_.nodes <= 1) return 0;
-  // make_keys + norms + quant (stage 1), fold + make_keys + norms + quant, decode
-  int k = 8;
-  if (impl_->flags & GCX_F_BIG_BUCKETS) k += 2;
-  return k;
+  // per encode (stage 1, owner re-encode): make_keys + K1b (+ norm pre-pass,
+  // big-bucket norms, generic K1b as the flags require); fold; decode
+  int enc = 2;
+  if (impl_->flags & GCX_F_NORM_PASS) ++enc;
+  if (impl_->flags & GCX_F_BIG_BUCKETS) ++enc;
+  if (impl_->flags & GCX_F_ODD_BUCKETS) ++enc;
+  return 2 * enc + 2;
 }
 
 }  // namespace gcomm::collectives

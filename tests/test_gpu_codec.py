@@ -175,3 +175,65 @@ def test_key_table_encode_matches_inline(dev, oracle):
         got_n = outs[1][p.norms:p.norms + 4 * wn.size].view(np.float32)
         assert (got_n.view(np.uint32) == wn.view(np.uint32)).all()
         assert (outs[1][p.packed:p.packed + wp.size] == wp).all()
+
+
+@pytest.mark.parametrize("bits", [1, 2, 4, 5, 8])
+@pytest.mark.parametrize("bucket", [32, 64, 96, 128, 256, 2048, 8192])
+def test_dense_fast_paths_vs_oracle(dev, oracle, bits, bucket):
+    """Zero-free inputs keep every group on K1b's 32-bit-compare fast path
+    (bucket % 32 == 0: fused norms for 32/64/128, pre-pass otherwise) and K3's
+    lane-per-chunk table path; ragged lengths end in a partial group."""
+    rng = np.random.default_rng(bits * 131 + bucket)
+    n = int(rng.integers(bucket, 70000)) | 1
+    v = (rng.standard_normal(n) * 10.0 ** rng.integers(-20, 20)).astype(np.float32)
+    v[v == 0] = np.float32(1e-3)
+    seed = int(rng.integers(0, 2**63))
+    norms, packed, deq = _gpu_codec(dev, v, bits, bucket, seed)
+    wn, wp = oracle.quantize(v, bits, bucket, seed)
+    assert (norms.view(np.uint32) == wn.view(np.uint32)).all()
+    assert (packed == wp).all()
+    wd = oracle.dequantize(wn, wp, n, bits, bucket)
+    assert (deq.view(np.uint32) == wd.view(np.uint32)).all()
+
+
+@pytest.mark.parametrize("bits", [2, 4, 7])
+def test_ambiguous_key_compare_takes_exact_path(dev, oracle, bits):
+    """K1b decides `uniform01 < p` on the key's top 32 bits and recomputes a
+    group whose top word equals floor(frac(x) * 2^32).  Build such an element:
+    bucket norm 1.0 (one dominant element), v0 tiny so x = v0 * s exactly, and
+    v0 chosen so floor(x * 2^32) is the key's top word."""
+    from paper_2111_08617_b200 import _capi
+    v, hh, k53, seed = _ambiguous_vector(_capi.lib(), bits, 0x1234567 + bits)
+    s = (1 << bits) - 1
+    x = float(v[0]) * s
+    assert int(np.floor(x * 2.0**32)) == hh  # the constructed tie on the top word
+    norms, packed, deq = _gpu_codec(dev, v, bits, 128, seed)
+    wn, wp = oracle.quantize(v, bits, 128, seed)
+    assert wn[0] == np.float32(1.0)
+    assert (packed == wp).all()
+    # and the decision itself: level 0 rounds up iff k53 < x * 2^53
+    up = k53 < x * 2.0**53
+    assert (int(wp[0]) & s) == (1 if up else 0)
+
+
+def _ambiguous_vector(lib, bits, seed, bucket=128):
+    """-> (v, hh, k53, seed): element 0 of bucket 0 ties on the key's top word.
+    The seed is advanced until the tie needs v0 < 2^-12, so the bucket norm
+    stays exactly 1.0 and x = v0 * s is exact."""
+    s = (1 << bits) - 1
+    while True:
+        k53 = int(lib.gcx_uniform01(seed, 0, 0) * 2.0**53)  # bucket 0, element 0
+        hh = k53 >> 21
+        if 0 < hh < min(s << 20, 1 << 22):  # float steps of v0 finer than the tie window
+            break
+        seed += 1
+    v0 = np.float32((hh + 0.5) / s / 2.0**32)
+    for _ in range(4096):  # walk to a float with floor(v0 * s * 2^32) == hh
+        fl = int(np.floor(float(v0) * s * 2.0**32))
+        if fl == hh:
+            break
+        v0 = np.nextafter(v0, np.float32(np.inf) if fl < hh else np.float32(0))
+    v = np.full(bucket, np.float32(1e-12))
+    v[0] = v0
+    v[1] = np.float32(1.0)
+    return v, hh, k53, seed

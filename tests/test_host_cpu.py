@@ -45,7 +45,9 @@ def test_capi_host_helpers(oracle):
     nt, prefix, flags = _capi.plan_tiles([_capi.Piece(0, 10000, 0, 0, 0, 128, 4)])
     assert nt == 3 and prefix == [0, 3] and flags == 0
     nt, _, flags = _capi.plan_tiles([_capi.Piece(0, 10000, 0, 0, 0, 1000, 4)])
-    assert flags == 0  # 4000-element tiles x 5 bits = 625 whole words
+    # 4000-element tiles x 5 bits = 625 whole words: no zeroing; bucket 1000 takes
+    # the generic K1b and the norm pre-pass
+    assert flags == _capi.GCX_F_ODD_BUCKETS | _capi.GCX_F_NORM_PASS
     nt, _, flags = _capi.plan_tiles([_capi.Piece(0, 10000, 0, 0, 0, 999, 4)])
     assert flags & _capi.GCX_F_NEEDS_ZERO  # 3996-element tiles x 5 bits straddle words
     _, _, flags = _capi.plan_tiles([_capi.Piece(0, 10000, 0, 0, 0, 5000, 4)])
