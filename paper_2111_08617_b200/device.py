@@ -31,7 +31,7 @@ def alloc_compressed(n: int, bits: int, bucket: int, device="cuda"):
 
 
 def quantize(x: torch.Tensor, bits: int, bucket: int, seed: int, norms=None, packed=None,
-             bad=None, stream=None):
+             bad=None, stream=None, reset_bad=True):
     """K1.  Returns (norms f32[nb], packed u8[capacity], bad u64[1]).
 
     ``bad`` holds UINT64_MAX unless a non-finite input was seen; then its low
@@ -42,6 +42,8 @@ def quantize(x: torch.Tensor, bits: int, bucket: int, seed: int, norms=None, pac
         norms, packed = alloc_compressed(n, bits, bucket, x.device)
     if bad is None:
         bad = torch.full((1,), -1, dtype=torch.int64, device=x.device)
+    elif not reset_bad:
+        pass  # the caller preset it to UINT64_MAX
     elif stream is not None:
         with torch.cuda.stream(stream):
             bad.fill_(-1)
