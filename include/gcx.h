@@ -46,6 +46,7 @@ extern "C" {
 #define GCX_F_PIECE_SEEDS 4u   /* use gcx_piece.seed instead of the launch seed */
 #define GCX_F_ODD_BUCKETS 8u   /* some quantized piece has bucket % 32 != 0: generic K1b */
 #define GCX_F_NORM_PASS 16u    /* some piece's norms come from the K1a pre-pass (bucket not 32/64/128) */
+#define GCX_F_LANE_GROUP 32u   /* some piece has bucket % 32 == 0 other than 32/64/128 (k_quant32) */
 
 #define GCX_TILE 4096          /* max elements per CTA tile */
 
@@ -62,8 +63,12 @@ typedef struct gcx_piece {
                       (gcx_plan_keys), or UINT64_MAX: draw keys inline */
 } gcx_piece;
 
-/* One run of a key table: keys[off + i] = the uniform01 key of piece-local
- * index i (< len) for bucket size `bucket` (util.hpp:26-29 before the >> 11). */
+/* One run of a key table: slot off + i holds the uniform01 key of piece-local
+ * index i (< len) for bucket size `bucket` (util.hpp:26-29 before the >> 11).
+ * Runs start on multiples of 1024 slots; a table of `total` slots occupies
+ * total * 8 bytes, laid out for coalesced reads by the quantizer (the high
+ * and low key words of each 1024-slot block are stored apart, gcx_kernels.cu
+ * key_pos). */
 typedef struct gcx_keygroup {
   uint64_t off;
   uint64_t len;
@@ -129,8 +134,8 @@ int gcx_decode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint
  * the owner's decoded result (divided by divisor) to out
  * (collectives.cpp:283-292). */
 int gcx_fold_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
-                    uint32_t ntiles, const uint8_t* recv, uint64_t slot_stride, const float* own,
-                    uint32_t nodes, uint32_t me, float* out, void* stream);
+                    uint32_t ntiles, uint32_t flags, const uint8_t* recv, uint64_t slot_stride,
+                    const float* own, uint32_t nodes, uint32_t me, float* out, void* stream);
 int gcx_sra_reduce(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
                    uint32_t ntiles, uint32_t flags, const uint8_t* recv, uint64_t slot_stride,
                    const float* own, uint32_t nodes, uint32_t me, uint64_t seed,

@@ -18,6 +18,7 @@ GCX_F_NEEDS_ZERO = 2
 GCX_F_PIECE_SEEDS = 4
 GCX_F_ODD_BUCKETS = 8
 GCX_F_NORM_PASS = 16
+GCX_F_LANE_GROUP = 32
 GCX_TILE = 4096
 
 
@@ -75,7 +76,7 @@ _decl("gcx_encode_pieces", i32, vp, vp, u32, u32, u32, u64, vp, vp, vp, vp, vp)
 _decl("gcx_decode_pieces", i32, vp, vp, u32, u32, u32, vp, vp, C.c_float, vp)
 _decl("gcx_plan_keys", i64, C.POINTER(Piece), u32, C.POINTER(KeyGroup), u32, C.POINTER(u32))
 _decl("gcx_make_keys", i32, vp, u32, u64, u64, vp, vp)
-_decl("gcx_fold_pieces", i32, vp, vp, u32, u32, vp, u64, vp, u32, u32, vp, vp)
+_decl("gcx_fold_pieces", i32, vp, vp, u32, u32, u32, vp, u64, vp, u32, u32, vp, vp)
 _decl("gcx_sra_reduce", i32, vp, vp, u32, u32, u32, vp, u64, vp, u32, u32, u64, vp, vp,
       C.c_float, vp, vp, vp)
 _decl("gcx_hash_bench", i32, u64, u64, u32, i32, vp, vp)

@@ -423,7 +423,7 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
   // owners: ascending-id fold into out, re-encode with the hop-1 seed
   for (std::size_t c = 0; c < N; ++c) {
     gcx_check(gcx_fold_pieces(blob.pieces(own[c]), blob.prefix(own[c]),
-                              std::uint32_t(own[c].pieces.size()), own[c].ntiles,
+                              std::uint32_t(own[c].pieces.size()), own[c].ntiles, own[c].flags,
                               mail.get<std::uint8_t>() + mbase[c], slot_stride[c],
                               in.get<float>() + c * d, std::uint32_t(N), std::uint32_t(c),
                               out.get<float>() + c * d, st));
@@ -582,7 +582,7 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
   // K2: ascending-id fold into out, then re-encode with the hop-1 seed
   std::uint8_t* bcast = I.gather_buf.get<std::uint8_t>() + layout_.gather_offset[me];
   gcx_check(gcx_fold_pieces(I.blob.pieces(I.own), I.blob.prefix(I.own),
-                            std::uint32_t(I.own.pieces.size()), I.own.ntiles,
+                            std::uint32_t(I.own.pieces.size()), I.own.ntiles, I.own.flags,
                             I.recv_buf.get<std::uint8_t>(), I.recv_stride, in, std::uint32_t(N),
                             std::uint32_t(me), out, st));
   encode(I.blob, I.own, hop_seed(step_seed, 1, me), out, bcast, keys, bad + 1, st);
@@ -629,6 +629,7 @@ int DeviceReducer::launches_per_call() const {
   // big-bucket norms, generic K1b as the flags require); fold; decode
   int enc = 2;
   if (impl_->flags & GCX_F_NORM_PASS) ++enc;
+  if (impl_->flags & GCX_F_LANE_GROUP) ++enc;
   if (impl_->flags & GCX_F_BIG_BUCKETS) ++enc;
   if (impl_->flags & GCX_F_ODD_BUCKETS) ++enc;
   return 2 * enc + 2;
