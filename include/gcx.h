@@ -47,6 +47,7 @@ extern "C" {
 #define GCX_F_ODD_BUCKETS 8u   /* some quantized piece has bucket % 32 != 0: generic K1b */
 #define GCX_F_NORM_PASS 16u    /* some piece's norms come from the K1a pre-pass (bucket not 32/64/128) */
 #define GCX_F_LANE_GROUP 32u   /* some piece has bucket % 32 == 0 other than 32/64/128 (k_quant32) */
+#define GCX_F_KEY_PREFIX 64u   /* the key table holds seed-independent prefixes (gcx_make_prefix) */
 
 #define GCX_TILE 4096          /* max elements per CTA tile */
 
@@ -99,6 +100,18 @@ int gcx_quantize(const float* x, uint64_t n, int bits, uint64_t bucket, uint64_t
                  float* norms, uint8_t* packed, unsigned long long* bad_key, void* stream);
 int gcx_dequantize(const float* norms, const uint8_t* packed, uint64_t n, int bits,
                    uint64_t bucket, float* out, void* stream);
+/* Key prefixes: the reference keys every draw as uniform01(seed, b, i) =
+ * mix64(seed ^ T(i)) >> 11 with T(i) = mix64(b ^ mix64(i)), b = i / bucket
+ * (util.hpp:26-29).  T depends only on (i, bucket), so a caller that
+ * quantizes same-shaped buffers every step (a gradient buffer) builds the
+ * table once and each step hashes one finalizer per element instead of
+ * three.  table: gcx_prefix_slots(n) entries of 8 bytes (laid out like a key
+ * table).  gcx_quantize_prefixed == gcx_quantize bit for bit. */
+uint64_t gcx_prefix_slots(uint64_t n);
+int gcx_make_prefix(uint64_t n, uint64_t bucket, unsigned long long* table, void* stream);
+int gcx_quantize_prefixed(const float* x, uint64_t n, int bits, uint64_t bucket, uint64_t seed,
+                          const unsigned long long* prefix, float* norms, uint8_t* packed,
+                          unsigned long long* bad_key, void* stream);
 
 /* ---- piece-table codec (device tables; tile_prefix from gcx_plan_tiles) ----
  * encode: src + pieces[k].src ... -> msg + pieces[k].norms/packed.  Raw pieces

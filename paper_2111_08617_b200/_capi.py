@@ -72,6 +72,9 @@ _decl("gcx_uniform01", C.c_double, u64, u64, u64)
 _decl("gcx_plan_tiles", i64, C.POINTER(Piece), u32, C.POINTER(u32), C.POINTER(u32))
 _decl("gcx_quantize", i32, vp, u64, i32, u64, u64, vp, vp, vp, vp)
 _decl("gcx_dequantize", i32, vp, vp, u64, i32, u64, vp, vp)
+_decl("gcx_prefix_slots", u64, u64)
+_decl("gcx_make_prefix", i32, u64, u64, vp, vp)
+_decl("gcx_quantize_prefixed", i32, vp, u64, i32, u64, u64, vp, vp, vp, vp, vp)
 _decl("gcx_encode_pieces", i32, vp, vp, u32, u32, u32, u64, vp, vp, vp, vp, vp)
 _decl("gcx_decode_pieces", i32, vp, vp, u32, u32, u32, vp, vp, C.c_float, vp)
 _decl("gcx_plan_keys", i64, C.POINTER(Piece), u32, C.POINTER(KeyGroup), u32, C.POINTER(u32))
@@ -86,7 +89,8 @@ EXPORTS = ["gcx_version", "gcx_last_error", "gcx_compressed_size", "gcx_packed_b
            "gcx_packed_capacity", "gcx_hop_seed", "gcx_uniform01", "gcx_plan_tiles",
            "gcx_quantize", "gcx_dequantize", "gcx_encode_pieces", "gcx_decode_pieces",
            "gcx_sra_reduce", "gcx_hash_bench", "gcx_device_info", "gcx_plan_keys",
-           "gcx_make_keys", "gcx_fold_pieces"]
+           "gcx_make_keys", "gcx_fold_pieces", "gcx_prefix_slots", "gcx_make_prefix",
+           "gcx_quantize_prefixed"]
 
 
 def lib():

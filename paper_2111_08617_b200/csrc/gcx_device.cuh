@@ -237,13 +237,22 @@ __device__ __forceinline__ void mix64_v(uint32_t& lo, uint32_t& hi, const HashK&
   xorshift_v<HV>(lo, hi, HV == 1 ? 31u : k.k31, k.m31);
 }
 
+// The seed-independent part of the key: T(i) = mix64(b ^ mix64(i)).
 template <int HV = GCX_HASH_HV>
-__device__ __forceinline__ uint32_t draw_key_hi(uint32_t i, uint32_t b, uint32_t s_lo,
-                                                uint32_t s_hi, const HashK& k) {
-  uint32_t lo = i, hi = 0u;
+__device__ __forceinline__ void draw_prefix(uint32_t i, uint32_t b, const HashK& k, uint32_t& lo,
+                                            uint32_t& hi) {
+  lo = i;
+  hi = 0u;
   mix64_v<HV>(lo, hi, k);
   lo ^= b;
   mix64_v<HV>(lo, hi, k);
+}
+
+// Top word of mix64(seed ^ T): the final `z ^= z >> 31` is applied to the
+// high word alone.
+template <int HV = GCX_HASH_HV>
+__device__ __forceinline__ uint32_t key_hi_from_prefix(uint32_t lo, uint32_t hi, uint32_t s_lo,
+                                                       uint32_t s_hi, const HashK& k) {
   lo ^= s_lo;
   hi ^= s_hi;
   asm("add.cc.u32 %0, %0, 0x7f4a7c15;\n\taddc.u32 %1, %1, 0x9e3779b9;" : "+r"(lo), "+r"(hi));
@@ -253,6 +262,17 @@ __device__ __forceinline__ uint32_t draw_key_hi(uint32_t i, uint32_t b, uint32_t
   // hi word of z * 0x94d049bb133111eb, then hi ^= hi >> 31
   const uint32_t h = __umulhi(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
   return h ^ shr_hi<HV>(h, HV == 1 ? 31u : k.k31, k.m31);
+}
+
+// top word of the uniform01 key of (seed, b, i); the low word is needed only
+// when the 32-bit comparison in quantize_field32 ties, and that path
+// recomputes the whole key
+template <int HV = GCX_HASH_HV>
+__device__ __forceinline__ uint32_t draw_key_hi(uint32_t i, uint32_t b, uint32_t s_lo,
+                                                uint32_t s_hi, const HashK& k) {
+  uint32_t lo, hi;
+  draw_prefix<HV>(i, b, k, lo, hi);
+  return key_hi_from_prefix<HV>(lo, hi, s_lo, s_hi, k);
 }
 
 // |v| (normal, non-zero float bits) as an exact double: exponent rebias only.

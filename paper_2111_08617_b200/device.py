@@ -55,6 +55,33 @@ def quantize(x: torch.Tensor, bits: int, bucket: int, seed: int, norms=None, pac
     return norms, packed, bad
 
 
+def make_prefix(n: int, bucket: int, device="cuda", stream=None) -> torch.Tensor:
+    """The seed-independent key prefixes T(i) of an n-element vector
+    (gcx_make_prefix); build once per buffer shape, reuse every step."""
+    table = torch.empty(_capi.lib().gcx_prefix_slots(n), dtype=torch.int64, device=device)
+    check(_capi.lib().gcx_make_prefix(n, bucket, table.data_ptr(), _stream_ptr(stream)))
+    return table
+
+
+def quantize_prefixed(x: torch.Tensor, bits: int, bucket: int, seed: int, prefix: torch.Tensor,
+                      norms=None, packed=None, bad=None, stream=None, reset_bad=True):
+    """K1 with a prefix table: bit-identical to ``quantize``."""
+    assert x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
+    n = x.numel()
+    if norms is None or packed is None:
+        norms, packed = alloc_compressed(n, bits, bucket, x.device)
+    if bad is None:
+        bad = torch.full((1,), -1, dtype=torch.int64, device=x.device)
+    elif reset_bad:
+        with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
+            bad.fill_(-1)
+    check(_capi.lib().gcx_quantize_prefixed(x.data_ptr(), n, bits, bucket, seed & _U64_MAX,
+                                            prefix.data_ptr(), norms.data_ptr(),
+                                            packed.data_ptr(), bad.data_ptr(),
+                                            _stream_ptr(stream)))
+    return norms, packed, bad
+
+
 def check_finite(bad: torch.Tensor) -> None:
     v = int(bad.item()) & _U64_MAX
     if v != _U64_MAX:

@@ -18,6 +18,13 @@ def load(path):
     lib.gcx_quantize.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.gcx_quantize.restype = C.c_int
+    lib.gcx_quantize_prefixed.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64,
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p]
+    lib.gcx_quantize_prefixed.restype = C.c_int
+    lib.gcx_make_prefix.argtypes = [C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]
+    lib.gcx_prefix_slots.argtypes = [C.c_uint64]
+    lib.gcx_prefix_slots.restype = C.c_uint64
     return lib
 
 
@@ -38,9 +45,18 @@ def main():
     out = {}
     for path in libs:
         lib = load(path)
+        prefix = torch.empty(lib.gcx_prefix_slots(n), dtype=torch.int64, device="cuda")
+        assert lib.gcx_make_prefix(n, bucket, prefix.data_ptr(), st.cuda_stream) == 0
+        use_prefix = os.environ.get("VARIANT_PREFIX", "1") == "1"
+
         def q(x, seed):
-            rc = lib.gcx_quantize(x.data_ptr(), n, bits, bucket, seed, norms.data_ptr(),
-                                  packed.data_ptr(), bad.data_ptr(), st.cuda_stream)
+            if use_prefix:
+                rc = lib.gcx_quantize_prefixed(x.data_ptr(), n, bits, bucket, seed,
+                                               prefix.data_ptr(), norms.data_ptr(),
+                                               packed.data_ptr(), bad.data_ptr(), st.cuda_stream)
+            else:
+                rc = lib.gcx_quantize(x.data_ptr(), n, bits, bucket, seed, norms.data_ptr(),
+                                      packed.data_ptr(), bad.data_ptr(), st.cuda_stream)
             assert rc == 0
         for k in range(5):
             q(xs[k % 4], 42)

@@ -237,3 +237,27 @@ def _ambiguous_vector(lib, bits, seed, bucket=128):
     v[0] = v0
     v[1] = np.float32(1.0)
     return v, hh, k53, seed
+
+
+@pytest.mark.parametrize("bits,bucket,n,zeros", [
+    (4, 128, 100_003, False), (4, 128, 65_537, True), (1, 32, 40_000, False),
+    (8, 64, 33_333, True), (3, 512, 70_001, False), (5, 96, 50_000, True),
+    (2, 1000, 30_000, False), (6, 8192, 50_000, False)])
+def test_prefixed_quantize_matches_oracle(dev, oracle, bits, bucket, n, zeros):
+    """gcx_quantize_prefixed (seed-independent key prefixes T(i) built once)
+    is bit-identical to the reference codec for every kernel route: fused
+    lane-per-bucket (32/64/128), pre-pass + lane-per-group (512, 8192),
+    generic (96 is 32-aligned: lane-per-group; 1000: generic k_quant)."""
+    rng = np.random.default_rng(bits * 1009 + bucket + n)
+    v = (rng.standard_normal(n) * 10.0 ** rng.integers(-8, 8)).astype(np.float32)
+    if zeros:
+        v[rng.random(n) < 0.01] = 0.0
+    x = torch.from_numpy(v).cuda()
+    prefix = dev.make_prefix(n, bucket)
+    for seed in (int(rng.integers(0, 2**63)), 7):
+        norms, packed, bad = dev.quantize_prefixed(x, bits, bucket, seed, prefix)
+        torch.cuda.synchronize()
+        dev.check_finite(bad)
+        wn, wp = oracle.quantize(v, bits, bucket, seed)
+        assert (norms.cpu().numpy().view(np.uint32) == wn.view(np.uint32)).all()
+        assert (packed.cpu().numpy()[: wp.size] == wp).all()
