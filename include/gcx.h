@@ -134,6 +134,14 @@ int64_t gcx_plan_keys(gcx_piece* pieces, uint32_t npieces, gcx_keygroup* groups,
                       uint32_t group_cap, uint32_t* ngroups);
 int gcx_make_keys(const gcx_keygroup* groups, uint32_t ngroups, uint64_t total, uint64_t seed,
                   unsigned long long* keys, void* stream);
+/* The same table in two steps for layouts that are reused every step (an
+ * SRA reducer): make_key_prefix stores the seed-independent T(slot) once;
+ * make_keys_prefixed then derives the step's keys with one finalizer per
+ * slot (key = mix64(seed ^ T), util.hpp:26-29).  Identical keys. */
+int gcx_make_key_prefix(const gcx_keygroup* groups, uint32_t ngroups, uint64_t total,
+                        unsigned long long* prefix, void* stream);
+int gcx_make_keys_prefixed(uint64_t total, uint64_t seed, const unsigned long long* prefix,
+                           unsigned long long* keys, void* stream);
 int gcx_decode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
                       uint32_t ntiles, uint32_t flags, const uint8_t* msg, float* dst,
                       float divisor, void* stream);

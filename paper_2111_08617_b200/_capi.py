@@ -79,6 +79,8 @@ _decl("gcx_encode_pieces", i32, vp, vp, u32, u32, u32, u64, vp, vp, vp, vp, vp)
 _decl("gcx_decode_pieces", i32, vp, vp, u32, u32, u32, vp, vp, C.c_float, vp)
 _decl("gcx_plan_keys", i64, C.POINTER(Piece), u32, C.POINTER(KeyGroup), u32, C.POINTER(u32))
 _decl("gcx_make_keys", i32, vp, u32, u64, u64, vp, vp)
+_decl("gcx_make_key_prefix", i32, vp, u32, u64, vp, vp)
+_decl("gcx_make_keys_prefixed", i32, u64, u64, vp, vp, vp)
 _decl("gcx_fold_pieces", i32, vp, vp, u32, u32, u32, vp, u64, vp, u32, u32, vp, vp)
 _decl("gcx_sra_reduce", i32, vp, vp, u32, u32, u32, vp, u64, vp, u32, u32, u64, vp, vp,
       C.c_float, vp, vp, vp)
@@ -90,7 +92,7 @@ EXPORTS = ["gcx_version", "gcx_last_error", "gcx_compressed_size", "gcx_packed_b
            "gcx_quantize", "gcx_dequantize", "gcx_encode_pieces", "gcx_decode_pieces",
            "gcx_sra_reduce", "gcx_hash_bench", "gcx_device_info", "gcx_plan_keys",
            "gcx_make_keys", "gcx_fold_pieces", "gcx_prefix_slots", "gcx_make_prefix",
-           "gcx_quantize_prefixed"]
+           "gcx_quantize_prefixed", "gcx_make_key_prefix", "gcx_make_keys_prefixed"]
 
 
 def lib():

@@ -303,11 +303,14 @@ struct TableBlob {
 
 // K1 over a table quantized under one seed: draw the shared key runs once
 // (gcx_make_keys), then norms + quantize + pack reading keys from the table
+// (from the table's stored key prefixes when given: one finalizer per slot)
 void encode(const TableBlob& blob, const Table& t, std::uint64_t seed, const float* src,
             std::uint8_t* msg, unsigned long long* keys, unsigned long long* bad,
-            cudaStream_t st) {
+            cudaStream_t st, const unsigned long long* key_prefix = nullptr) {
   const bool use_keys = keys != nullptr && t.key_len > 0;
-  if (use_keys)
+  if (use_keys && key_prefix != nullptr)
+    gcx_check(gcx_make_keys_prefixed(t.key_len, seed, key_prefix, keys, st));
+  else if (use_keys)
     gcx_check(gcx_make_keys(blob.groups(t), std::uint32_t(t.groups.size()), t.key_len, seed, keys,
                             st));
   gcx_check(gcx_encode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
@@ -409,6 +412,17 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
     cuda_check(cudaMemsetAsync(mail.get(), 0, mail.size(), st), "memset");
     cuda_check(cudaMemsetAsync(gather.get(), 0, gather.size(), st), "memset");
   }
+  // each node's persistent state, as a DeviceReducer holds it: the
+  // seed-independent key prefixes of its send and owner tables
+  std::vector<DeviceBuffer> kpre(2 * N);
+  for (std::size_t k = 0; k < N; ++k) {
+    const Table* tt[2] = {&send[k], &own[k]};
+    for (int r = 0; r < 2; ++r) {
+      kpre[2 * k + r].reset(8 * tt[r]->key_len + 16);
+      gcx_check(gcx_make_key_prefix(blob.groups(*tt[r]), std::uint32_t(tt[r]->groups.size()),
+                                    tt[r]->key_len, kpre[2 * k + r].get<unsigned long long>(), st));
+    }
+  }
   cudaEvent_t e0, e1;
   cuda_check(cudaEventCreate(&e0), "event");
   cuda_check(cudaEventCreate(&e1), "event");
@@ -419,7 +433,7 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
   // stage 1 (scatter): every sender encodes its share of every other chunk
   for (std::size_t id = 0; id < N; ++id)
     encode(blob, send[id], hop_seed(req.step_seed, 0, id), in.get<float>() + id * d,
-           mail.get<std::uint8_t>(), kp, badp + id, st);
+           mail.get<std::uint8_t>(), kp, badp + id, st, kpre[2 * id].get<unsigned long long>());
   // owners: ascending-id fold into out, re-encode with the hop-1 seed
   for (std::size_t c = 0; c < N; ++c) {
     gcx_check(gcx_fold_pieces(blob.pieces(own[c]), blob.prefix(own[c]),
@@ -428,7 +442,8 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
                               in.get<float>() + c * d, std::uint32_t(N), std::uint32_t(c),
                               out.get<float>() + c * d, st));
     encode(blob, own[c], hop_seed(req.step_seed, 1, c), out.get<float>() + c * d,
-           gather.get<std::uint8_t>() + L.gather_offset[c], kp, badp + N + c, st);
+           gather.get<std::uint8_t>() + L.gather_offset[c], kp, badp + N + c, st,
+           kpre[2 * c + 1].get<unsigned long long>());
   }
   // stage 2 (all-gather): everyone decodes every owner's bytes (own included)
   for (std::size_t id = 0; id < N; ++id)
@@ -484,6 +499,7 @@ struct DeviceReducer::Impl {
   Table send, own, dec;
   TableBlob blob;
   DeviceBuffer send_buf, recv_buf, gather_buf, bad, keys;
+  DeviceBuffer prefix_send, prefix_own;  // seed-independent key prefixes, built once
   std::uint64_t recv_stride = 0;
   std::uint32_t flags = 0;
 };
@@ -527,6 +543,13 @@ DeviceReducer::DeviceReducer(Communicator& comm, std::size_t d, std::vector<Segm
   I.flags = I.send.flags | I.own.flags;
   I.blob.upload({&I.send, &I.own, &I.dec});
   I.keys.reset(8 * std::max(I.send.key_len, I.own.key_len) + 16);
+  I.prefix_send.reset(8 * I.send.key_len + 16);
+  I.prefix_own.reset(8 * I.own.key_len + 16);
+  gcx_check(gcx_make_key_prefix(I.blob.groups(I.send), std::uint32_t(I.send.groups.size()),
+                                I.send.key_len, I.prefix_send.get<unsigned long long>(), nullptr));
+  gcx_check(gcx_make_key_prefix(I.blob.groups(I.own), std::uint32_t(I.own.groups.size()),
+                                I.own.key_len, I.prefix_own.get<unsigned long long>(), nullptr));
+  cuda_check(cudaDeviceSynchronize(), "key prefixes");
   I.recv_stride = align_up(std::max<std::uint64_t>(layout_.chunks[me].msg_bytes, 16), kMsgAlign);
   I.send_buf.reset(layout_.gather_bytes + 16);
   I.gather_buf.reset(layout_.gather_bytes + 16);
@@ -562,7 +585,7 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
   auto* keys = I.keys.get<unsigned long long>();
   // K1: my share of every other owner's chunk, seed hop_seed(step, 0, me)
   encode(I.blob, I.send, hop_seed(step_seed, 0, me), in, I.send_buf.get<std::uint8_t>(), keys,
-         bad, st);
+         bad, st, I.prefix_send.get<unsigned long long>());
   // round 1: all-to-all of compressed chunks
   const std::uint64_t m_me = layout_.chunks[me].msg_bytes;
   nccl_check(ncclGroupStart(), "ncclGroupStart");
@@ -585,7 +608,8 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
                             std::uint32_t(I.own.pieces.size()), I.own.ntiles, I.own.flags,
                             I.recv_buf.get<std::uint8_t>(), I.recv_stride, in, std::uint32_t(N),
                             std::uint32_t(me), out, st));
-  encode(I.blob, I.own, hop_seed(step_seed, 1, me), out, bcast, keys, bad + 1, st);
+  encode(I.blob, I.own, hop_seed(step_seed, 1, me), out, bcast, keys, bad + 1, st,
+         I.prefix_own.get<unsigned long long>());
   // round 2: variable-size all-gather of the owners' compressed aggregates
   nccl_check(ncclGroupStart(), "ncclGroupStart");
   for (std::size_t j = 1; j < N; ++j) {
@@ -632,7 +656,8 @@ int DeviceReducer::launches_per_call() const {
   if (impl_->flags & GCX_F_LANE_GROUP) ++enc;
   if (impl_->flags & GCX_F_BIG_BUCKETS) ++enc;
   if (impl_->flags & GCX_F_ODD_BUCKETS) ++enc;
-  return 2 * enc + 2;
+  const int odd = (impl_->flags & GCX_F_ODD_BUCKETS) ? 1 : 0;  // generic fold / decode too
+  return 2 * enc + 2 * (1 + odd);
 }
 
 }  // namespace gcomm::collectives
