@@ -154,6 +154,31 @@ def test_key_table_encode_matches_inline(dev, oracle):
     st = torch.cuda.current_stream().cuda_stream
     _capi.check(_capi.lib().gcx_make_keys(dev_groups.data_ptr(), ng.value, total, seed,
                                           keys.data_ptr(), st))
+    # the two-step form an SRA reducer uses: stored prefixes, then one
+    # finalizer per slot per step -> the same table word for word
+    kpre = torch.empty(total, dtype=torch.int64, device="cuda")
+    keys2 = torch.empty(total, dtype=torch.int64, device="cuda")
+    _capi.check(_capi.lib().gcx_make_key_prefix(dev_groups.data_ptr(), ng.value, total,
+                                                kpre.data_ptr(), st))
+    _capi.check(_capi.lib().gcx_make_keys_prefixed(total, seed, kpre.data_ptr(), keys2.data_ptr(),
+                                                   st))
+    torch.cuda.synchronize()
+    k1 = keys.cpu().numpy().view(np.uint32)
+    k2 = keys2.cpu().numpy().view(np.uint32)
+    for g in range(ng.value):  # every slot a piece can read (run padding is never read)
+        t = groups[g].off + np.arange(groups[g].len, dtype=np.int64)
+        pos = ((t >> 10) << 11) | (((t & 31) >> 2) << 7) | (((t >> 5) & 31) << 2) | (t & 3)
+        assert (k1[pos] == k2[pos]).all() and (k1[pos + 1024] == k2[pos + 1024]).all()
+    # spot-check table words against the reference RNG: slot s of run g holds
+    # uniform01's key of piece-local index i = s - off (high word at key_pos)
+    kw = keys.cpu().numpy().view(np.uint32)
+    for g in range(ng.value):
+        grp = groups[g]
+        for i in (0, 1, 33, grp.len - 1):
+            t = grp.off + i
+            pos = ((t >> 10) << 11) | (((t & 31) >> 2) << 7) | (((t >> 5) & 31) << 2) | (t & 3)
+            k53 = (int(kw[pos]) << 32 | int(kw[pos + 1024])) >> 11
+            assert k53 * 2.0**-53 == _capi.lib().gcx_uniform01(seed, i // grp.bucket, i)
     outs = []
     for use_keys in (False, True):
         msg = torch.zeros(off + 64, dtype=torch.uint8, device="cuda")
