@@ -283,6 +283,24 @@ def run_codec(args):
         torch.cuda.synchronize()
         hash_ms[variant] = h0.elapsed_time(h1) / 5
 
+    # K4 (adaptive statistics, adaptive.cpp:21-35): the per-step FP64 window
+    # accumulate sum[i] += (double)g[i] over the same 25.6 M gradient
+    from paper_2111_08617_b200 import _capi
+    wsum = torch.zeros(n, dtype=torch.float64, device="cuda")
+    nonfin = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for k in range(3):
+        _capi.check(_capi.lib().gcx_stats_accumulate(wsum.data_ptr(), sets[k % nsets][0].data_ptr(),
+                                                     n, nonfin.data_ptr(), stream.cuda_stream))
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for k in range(args.steps):
+        _capi.check(_capi.lib().gcx_stats_accumulate(wsum.data_ptr(), sets[k % nsets][0].data_ptr(),
+                                                     n, nonfin.data_ptr(), stream.cuda_stream))
+    a1.record(stream)
+    torch.cuda.synchronize()
+    acc_ms = a0.elapsed_time(a1) / args.steps
+    del wsum
+
     # end to end through the C-ABI with host buffers: every step copies its
     # input from pinned host memory (H2D), runs gcx_quantize + gcx_dequantize
     # and reads the result back (D2H).  Steps are double-buffered over three
@@ -317,6 +335,10 @@ def run_codec(args):
                            "once per buffer shape (gcx_make_prefix, outside the timed region); "
                            "each step hashes mix64(seed ^ T(i)) with a fresh seed",
                    "quantize_inline_ms": q_inline_ms,
+                   "k4_window_accumulate_ms": acc_ms,
+                   "k4_window_accumulate_GBps": 20 * n / (acc_ms * 1e-3) / 1e9,
+                   "k4_note": "adaptive statistics: sum[i] += (double)g[i] (read 4+8 B, write 8 B "
+                              "per element), once per step inside observation windows",
                    "quantize_GBps_algorithmic": achieved,
                    "dequantize_GBps_algorithmic": q_bytes / (dq_ms * 1e-3) / 1e9,
                    "hash_only_ms": {f"variant{k}": v for k, v in hash_ms.items()},

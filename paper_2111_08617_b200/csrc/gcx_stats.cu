@@ -28,8 +28,29 @@ thread_local std::string g_err2;
 
 __global__ void k_accumulate(double* __restrict__ sum, const float* __restrict__ v, uint64_t n,
                              unsigned int* __restrict__ nonfinite) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t t0 = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  uint64_t head = 0;
+  if (((reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(sum)) & 15u) == 0) {
+    // 16-byte accesses: one float4 of the gradient, two double2 of the sums
+    const uint64_t n4 = n >> 2;
+    const float4* v4 = reinterpret_cast<const float4*>(v);
+    double2* s2 = reinterpret_cast<double2*>(sum);
+    for (uint64_t q = t0; q < n4; q += stride) {
+      const float4 x = __ldcs(v4 + q);
+      double2 a = s2[2 * q], b = s2[2 * q + 1];
+      if (!(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w)))
+        atomicOr(nonfinite, 1u);
+      a.x = __dadd_rn(a.x, double(x.x));
+      a.y = __dadd_rn(a.y, double(x.y));
+      b.x = __dadd_rn(b.x, double(x.z));
+      b.y = __dadd_rn(b.y, double(x.w));
+      s2[2 * q] = a;
+      s2[2 * q + 1] = b;
+    }
+    head = n4 << 2;
+  }
+  for (uint64_t i = head + t0; i < n; i += stride) {
     const float x = v[i];
     if (!isfinite(x)) atomicOr(nonfinite, 1u);
     sum[i] = __dadd_rn(sum[i], double(x));
