@@ -163,6 +163,10 @@ int gcx_sra_reduce(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_
                    uint8_t* bcast, float* out, float divisor, const unsigned long long* keys,
                    unsigned long long* bad_key, void* stream);
 
+/* acc[i] = acc[i] + x[i] in f32 (the ring and tree topologies' folds,
+ * collectives.cpp:359-361 and :412-413). */
+int gcx_add_f32(float* acc, const float* x, uint64_t n, void* stream);
+
 /* ---- microbenchmarks ----
  * Integer ceiling of the reference RNG: n draws of uniform01(seed, i/bucket, i),
  * xor-reduced into *sink (device u64).  variant 0 = reference 64-bit form,

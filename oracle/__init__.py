@@ -244,6 +244,10 @@ class RefOracle:
                                      C.POINTER(flt)]
         L.ref_serialize.restype = u64
         L.ref_serialize.argtypes = [C.POINTER(flt), u64, C.c_int, u64, u64, C.POINTER(C.c_uint8)]
+        L.ref_allreduce_topo.restype = C.c_int
+        L.ref_allreduce_topo.argtypes = [C.POINTER(C.POINTER(flt)), u64, u64, C.POINTER(Segment),
+                                         u64, u64, C.c_int, C.c_int, C.POINTER(C.POINTER(flt)),
+                                         C.POINTER(u64), C.POINTER(u64)]
         L.ref_allreduce.restype = C.c_int
         L.ref_allreduce.argtypes = [C.POINTER(C.POINTER(flt)), u64, u64, C.POINTER(Segment), u64,
                                     u64, C.c_int, C.POINTER(C.POINTER(flt)), C.POINTER(u64),
@@ -282,16 +286,17 @@ class RefOracle:
         n = self.lib.ref_serialize(_f32p(v), v.size, bits, bucket, seed, _u8p(out))
         return out[:n]
 
-    def allreduce(self, inputs, segments, step_seed, average=True):
+    def allreduce(self, inputs, segments, step_seed, average=True, topology="sra"):
         """-> (outputs per node, bytes_sent per node, counters dict)."""
         inputs = [np.ascontiguousarray(x, np.float32) for x in inputs]
         nodes, d = len(inputs), inputs[0].size
         outs = [np.empty(d, np.float32) for _ in range(nodes)]
         sent = (C.c_uint64 * nodes)()
         ctr = (C.c_uint64 * 5)()
-        self._check(self.lib.ref_allreduce(_ptrs(inputs), nodes, d, _segs(segments),
-                                           len(segments), step_seed, 1 if average else 0,
-                                           _ptrs(outs), sent, ctr))
+        topo = {"sra": 0, "ring": 1, "tree": 2}[topology]
+        self._check(self.lib.ref_allreduce_topo(_ptrs(inputs), nodes, d, _segs(segments),
+                                                len(segments), step_seed, 1 if average else 0,
+                                                topo, _ptrs(outs), sent, ctr))
         keys = ["compress_calls", "decompress_calls", "message_count", "rounds",
                 "max_compress_depth"]
         return outs, list(sent), dict(zip(keys, list(ctr)))

@@ -82,9 +82,23 @@ std::uint64_t ref_serialize(const float* v, std::uint64_t n, int bits, std::uint
 
 // SRA allreduce through the reference's SimNet with `nodes` threads.
 // outputs: nodes pointers to d floats. bytes_sent: nodes entries.
+int ref_allreduce_topo(const float* const* inputs, std::uint64_t nodes, std::uint64_t d,
+                       const ref_segment* segs, std::uint64_t nsegs, std::uint64_t step_seed,
+                       int op, int topology, float* const* outputs, std::uint64_t* bytes_sent,
+                       std::uint64_t* counters);
+
 int ref_allreduce(const float* const* inputs, std::uint64_t nodes, std::uint64_t d,
                   const ref_segment* segs, std::uint64_t nsegs, std::uint64_t step_seed, int op,
                   float* const* outputs, std::uint64_t* bytes_sent, std::uint64_t* counters) {
+  return ref_allreduce_topo(inputs, nodes, d, segs, nsegs, step_seed, op, 0, outputs, bytes_sent,
+                            counters);
+}
+
+// topology: 0 = sra, 1 = ring, 2 = tree (collectives.hpp Topology order)
+int ref_allreduce_topo(const float* const* inputs, std::uint64_t nodes, std::uint64_t d,
+                       const ref_segment* segs, std::uint64_t nsegs, std::uint64_t step_seed,
+                       int op, int topology, float* const* outputs, std::uint64_t* bytes_sent,
+                       std::uint64_t* counters) {
   try {
     gcomm::collectives::ReduceRequest req;
     req.inputs.resize(nodes);
@@ -98,7 +112,9 @@ int ref_allreduce(const float* const* inputs, std::uint64_t nodes, std::uint64_t
       seg.bucket_size = segs[s].bucket;
       req.segments.push_back(seg);
     }
-    req.topology = gcomm::collectives::Topology::sra;
+    req.topology = topology == 1   ? gcomm::collectives::Topology::ring
+                   : topology == 2 ? gcomm::collectives::Topology::tree
+                                   : gcomm::collectives::Topology::sra;
     req.op = op ? gcomm::collectives::ReduceOp::average : gcomm::collectives::ReduceOp::sum;
     req.step_seed = step_seed;
     gcomm::simnet::SimNetConfig cfg;

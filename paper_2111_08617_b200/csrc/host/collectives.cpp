@@ -342,6 +342,254 @@ void append(Table& t, const std::vector<gcx_piece>& src, std::uint64_t delta) {
   throw std::invalid_argument("non-finite gradient value at index " + std::to_string(local));
 }
 
+// quantized pieces of a piece list (for the reference's call counters)
+std::uint64_t quantized(const std::vector<gcx_piece>& ps) {
+  std::uint64_t q = 0;
+  for (const auto& p : ps) q += p.bits > 0 ? 1 : 0;
+  return q;
+}
+
+void encode_inline(const TableBlob& blob, const Table& t, std::uint64_t seed, const float* src,
+                   std::uint8_t* msg, std::uint64_t msg_bytes, unsigned long long* bad,
+                   cudaStream_t st) {
+  if (t.flags & GCX_F_NEEDS_ZERO)
+    cuda_check(cudaMemsetAsync(msg, 0, msg_bytes, st), "memset");
+  gcx_check(gcx_encode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
+                              t.ntiles, t.flags, seed, src, msg, nullptr, bad, st));
+}
+
+void decode_into(const TableBlob& blob, const Table& t, const std::uint8_t* msg, float* dst,
+                 float divisor, cudaStream_t st) {
+  gcx_check(gcx_decode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
+                              t.ntiles, t.flags, msg, dst, divisor, st));
+}
+
+// run_ring (collectives.cpp:312-386) with every node on this GPU: the
+// reduce-scatter carries a chunk around the ring, each stop decoding the
+// partial, adding its local values and re-encoding (hop seed (t, me)); the
+// owner encodes its finished chunk once (hop N-1) and the bytes travel
+// verbatim, so every node decodes the same payload.
+ReduceResult allreduce_ring(const ReduceRequest& req, std::size_t N) {
+  const std::size_t d = req.inputs[0].size();
+  const SraLayout L = make_layout(d, N, req.segments);
+  std::vector<Table> loc(N), full(N);
+  std::uint64_t max_msg = 16;
+  for (std::size_t c = 0; c < N; ++c) {
+    loc[c].pieces = L.chunks[c].pieces;
+    for (auto& p : loc[c].pieces) p.src -= L.bounds[c];  // chunk-local
+    full[c].pieces = L.chunks[c].pieces;                  // buffer offsets
+    loc[c].plan();
+    full[c].plan();
+    max_msg = std::max<std::uint64_t>(max_msg, L.chunks[c].msg_bytes);
+  }
+  std::vector<Table*> all;
+  for (std::size_t c = 0; c < N; ++c) {
+    all.push_back(&loc[c]);
+    all.push_back(&full[c]);
+  }
+  TableBlob blob;
+  blob.upload(all);
+  std::size_t max_chunk = 1;
+  for (std::size_t c = 0; c < N; ++c)
+    max_chunk = std::max(max_chunk, L.bounds[c + 1] - L.bounds[c]);
+  const std::uint64_t mstride = align_up(max_msg, kMsgAlign);
+
+  detail::Stream stream;
+  cudaStream_t st = stream.get();
+  DeviceBuffer in(4 * d * N + 16), out(4 * d * N + 16), carry(4 * max_chunk * N + 16),
+      msg(mstride * N + 16), gather(L.gather_bytes + 16), bad(8 * N * N + 16);
+  for (std::size_t k = 0; k < N; ++k)
+    cuda_check(cudaMemcpyAsync(in.get<float>() + k * d, req.inputs[k].data(), 4 * d,
+                               cudaMemcpyHostToDevice, st), "H2D");
+  cuda_check(cudaMemsetAsync(bad.get(), 0xFF, bad.size(), st), "memset");
+  cudaEvent_t e0, e1;
+  cuda_check(cudaEventCreate(&e0), "event");
+  cuda_check(cudaEventCreate(&e1), "event");
+  cudaEventRecord(e0, st);
+  auto chunk_at = [N](std::size_t j, std::size_t back) { return (j + N - back % N) % N; };
+  auto* badp = bad.get<unsigned long long>();
+  auto cbuf = [&](std::size_t me) { return carry.get<float>() + me * max_chunk; };
+  auto mbuf = [&](std::size_t me) { return msg.get<std::uint8_t>() + me * mstride; };
+  for (std::size_t me = 0; me < N; ++me) {
+    const std::size_t c = chunk_at(me, 1);
+    cuda_check(cudaMemcpyAsync(cbuf(me), in.get<float>() + me * d + L.bounds[c],
+                               4 * (L.bounds[c + 1] - L.bounds[c]), cudaMemcpyDeviceToDevice, st),
+               "D2D");
+  }
+  for (std::size_t t = 0; t + 1 < N; ++t) {
+    for (std::size_t me = 0; me < N; ++me) {  // every node sends right
+      const std::size_t c = chunk_at(me, 1 + t);
+      encode_inline(blob, loc[c], hop_seed(req.step_seed, t, me), cbuf(me), mbuf(me),
+                    L.chunks[c].msg_bytes, badp + t * N + me, st);
+    }
+    for (std::size_t me = 0; me < N; ++me) {  // and folds what came from the left
+      const std::size_t left = (me + N - 1) % N, c = chunk_at(me, 2 + t);
+      decode_into(blob, loc[c], mbuf(left), cbuf(me), 1.0f, st);
+      gcx_check(gcx_add_f32(cbuf(me), in.get<float>() + me * d + L.bounds[c],
+                            L.bounds[c + 1] - L.bounds[c], st));
+    }
+  }
+  const float divisor = req.op == ReduceOp::average ? float(N) : 1.0f;
+  for (std::size_t me = 0; me < N; ++me)  // owners: chunk me, hop N-1
+    encode_inline(blob, loc[me], hop_seed(req.step_seed, N - 1, me), cbuf(me),
+                  gather.get<std::uint8_t>() + L.gather_offset[me], L.chunks[me].msg_bytes,
+                  badp + (N - 1) * N + me, st);
+  for (std::size_t me = 0; me < N; ++me)
+    for (std::size_t c = 0; c < N; ++c)
+      decode_into(blob, full[c], gather.get<std::uint8_t>() + L.gather_offset[c],
+                  out.get<float>() + me * d, divisor, st);
+  cudaEventRecord(e1, st);
+  ReduceResult result;
+  result.outputs.assign(N, std::vector<float>(d));
+  for (std::size_t k = 0; k < N; ++k)
+    cuda_check(cudaMemcpyAsync(result.outputs[k].data(), out.get<float>() + k * d, 4 * d,
+                               cudaMemcpyDeviceToHost, st), "D2H");
+  std::vector<std::uint64_t> badh(N * N);
+  cuda_check(cudaMemcpyAsync(badh.data(), bad.get(), 8 * N * N, cudaMemcpyDeviceToHost, st), "D2H");
+  stream.sync();
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  for (std::size_t k = 0; k < N * N; ++k)
+    if (badh[k] != ~0ULL) throw_non_finite(loc[0], badh[k]);
+  // the reference's counters (collectives.cpp:340-384)
+  StepTrace tr;
+  tr.bytes_sent.assign(N, 0);
+  tr.bytes_received.assign(N, 0);
+  for (std::size_t me = 0; me < N; ++me) {
+    const std::size_t right = (me + 1) % N;
+    for (std::size_t t = 0; t + 1 < N; ++t) {
+      const std::uint64_t rs = L.chunks[chunk_at(me, 1 + t)].wire_bytes;  // reduce-scatter
+      const std::uint64_t ag = L.chunks[chunk_at(me, t)].wire_bytes;      // forwarded gather
+      tr.bytes_sent[me] += rs + ag;
+      tr.bytes_received[right] += rs + ag;
+      tr.compress_calls += quantized(L.chunks[chunk_at(me, 1 + t)].pieces);
+      tr.decompress_calls += quantized(L.chunks[chunk_at(me, 2 + t)].pieces) +
+                             quantized(L.chunks[chunk_at(me, 1 + t)].pieces);
+    }
+    tr.compress_calls += quantized(L.chunks[me].pieces);
+    tr.decompress_calls += quantized(L.chunks[me].pieces);
+  }
+  tr.message_count = 2 * N * (N - 1);
+  tr.rounds = 2 * (N - 1);
+  // compression depth as the reference propagates it (message notes)
+  {
+    auto q = [&](std::size_t c) -> std::uint64_t { return quantized(L.chunks[c].pieces) ? 1 : 0; };
+    std::vector<std::uint64_t> carry_d(N, 0), sent(N);
+    for (std::size_t t = 0; t + 1 < N; ++t) {
+      for (std::size_t me = 0; me < N; ++me) sent[me] = carry_d[me] + q(chunk_at(me, 1 + t));
+      for (std::size_t me = 0; me < N; ++me) carry_d[me] = sent[(me + N - 1) % N];
+    }
+    for (std::size_t me = 0; me < N; ++me)
+      tr.max_compress_depth = std::max(tr.max_compress_depth, carry_d[me] + q(me));
+  }
+  tr.device_time_s = ms * 1e-3;
+  result.trace = tr;
+  return result;
+}
+
+// run_tree (collectives.cpp:388-471): binary reduction toward node 0 with a
+// re-encode at every level (hop seed (level, me)), then the root encodes
+// once (hop `levels`) and every node decodes the same bytes.
+ReduceResult allreduce_tree(const ReduceRequest& req, std::size_t N) {
+  const std::size_t d = req.inputs[0].size();
+  const SraLayout L1 = make_layout(d, 1, req.segments);  // one chunk = the full piece list
+  Table full;
+  full.pieces = L1.chunks[0].pieces;
+  full.plan();
+  TableBlob blob;
+  blob.upload({&full});
+  std::size_t levels = 0;
+  while ((std::size_t{1} << levels) < N) ++levels;
+  const std::uint64_t mbytes = std::max<std::uint64_t>(L1.chunks[0].msg_bytes, 16);
+  const std::uint64_t mstride = align_up(mbytes, kMsgAlign);
+
+  detail::Stream stream;
+  cudaStream_t st = stream.get();
+  DeviceBuffer acc(4 * d * N + 16), tmp(4 * d + 16), msg(mstride * (N + 1) + 16),
+      out(4 * d * N + 16), bad(8 * (N + 1) + 16);
+  for (std::size_t k = 0; k < N; ++k)
+    cuda_check(cudaMemcpyAsync(acc.get<float>() + k * d, req.inputs[k].data(), 4 * d,
+                               cudaMemcpyHostToDevice, st), "H2D");
+  cuda_check(cudaMemsetAsync(bad.get(), 0xFF, bad.size(), st), "memset");
+  cudaEvent_t e0, e1;
+  cuda_check(cudaEventCreate(&e0), "event");
+  cuda_check(cudaEventCreate(&e1), "event");
+  cudaEventRecord(e0, st);
+  auto* badp = bad.get<unsigned long long>();
+  auto abuf = [&](std::size_t me) { return acc.get<float>() + me * d; };
+  auto mbuf = [&](std::size_t me) { return msg.get<std::uint8_t>() + me * mstride; };
+  std::vector<bool> sent(N, false);
+  for (std::size_t l = 0; l < levels; ++l) {
+    const std::size_t stride = std::size_t{1} << l, group = stride << 1;
+    for (std::size_t me = 0; me < N; ++me)
+      if (!sent[me] && me % group == stride) {
+        encode_inline(blob, full, hop_seed(req.step_seed, l, me), abuf(me), mbuf(me), mbytes,
+                      badp + me, st);
+        sent[me] = true;
+      }
+    for (std::size_t me = 0; me < N; ++me)
+      if (!sent[me] && me % group == 0 && me + stride < N) {
+        decode_into(blob, full, mbuf(me + stride), tmp.get<float>(), 1.0f, st);
+        gcx_check(gcx_add_f32(abuf(me), tmp.get<float>(), d, st));
+      }
+  }
+  const float divisor = req.op == ReduceOp::average ? float(N) : 1.0f;
+  encode_inline(blob, full, hop_seed(req.step_seed, levels, 0), abuf(0), mbuf(N), mbytes, badp + N,
+                st);
+  for (std::size_t me = 0; me < N; ++me)
+    decode_into(blob, full, mbuf(N), out.get<float>() + me * d, divisor, st);
+  cudaEventRecord(e1, st);
+  ReduceResult result;
+  result.outputs.assign(N, std::vector<float>(d));
+  for (std::size_t k = 0; k < N; ++k)
+    cuda_check(cudaMemcpyAsync(result.outputs[k].data(), out.get<float>() + k * d, 4 * d,
+                               cudaMemcpyDeviceToHost, st), "D2H");
+  std::vector<std::uint64_t> badh(N + 1);
+  cuda_check(cudaMemcpyAsync(badh.data(), bad.get(), 8 * (N + 1), cudaMemcpyDeviceToHost, st), "D2H");
+  stream.sync();
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  for (std::size_t k = 0; k <= N; ++k)
+    if (badh[k] != ~0ULL) throw_non_finite(full, badh[k]);
+  StepTrace tr;
+  tr.bytes_sent.assign(N, 0);
+  tr.bytes_received.assign(N, 0);
+  const std::uint64_t w = L1.chunks[0].wire_bytes, q = quantized(full.pieces);
+  for (std::size_t me = 1; me < N; ++me) {  // one upward message per non-root node
+    const std::size_t parent = me & (me - 1);
+    tr.bytes_sent[me] += w;
+    tr.bytes_received[parent] += w;
+    tr.bytes_sent[parent] += w;  // and the broadcast back down the same edge
+    tr.bytes_received[me] += w;
+  }
+  tr.message_count = 2 * (N - 1);
+  tr.rounds = 2 * levels;
+  {  // compression depth: upward notes, then the root's broadcast note
+    const std::uint64_t qq = q ? 1 : 0;
+    std::vector<std::uint64_t> depth(N, 0);
+    std::vector<bool> up(N, false);
+    for (std::size_t l = 0; l < levels; ++l) {
+      const std::size_t stride = std::size_t{1} << l, group = stride << 1;
+      for (std::size_t me = 0; me < N; ++me)
+        if (!up[me] && me % group == stride) {
+          up[me] = true;
+          tr.max_compress_depth = std::max(tr.max_compress_depth, depth[me] + qq);
+          depth[me - stride] = std::max(depth[me - stride], depth[me] + qq);
+        }
+    }
+    tr.max_compress_depth = std::max(tr.max_compress_depth, depth[0] + qq);
+  }
+  tr.compress_calls = N * q;
+  tr.decompress_calls = (2 * N - 1) * q;
+  tr.device_time_s = ms * 1e-3;
+  result.trace = tr;
+  return result;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -358,10 +606,9 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
     result.trace.bytes_received.assign(1, 0);
     return result;
   }
-  if (req.topology != Topology::sra)
-    throw std::invalid_argument("topology " + to_string(req.topology) +
-                                " is not on the B200 path (sra only)");
   detail::require_device();
+  if (req.topology == Topology::ring) return allreduce_ring(req, nodes);
+  if (req.topology == Topology::tree) return allreduce_tree(req, nodes);
   const std::size_t N = nodes, d = req.inputs[0].size();
   const SraLayout L = make_layout(d, N, req.segments);
 

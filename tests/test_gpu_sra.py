@@ -160,3 +160,44 @@ def test_determinism_and_seed_sensitivity(g, oracle):
     b = g.allreduce(_request(g, inputs, [(0, d, 0, 4, 128)], 11, True), nodes).outputs[0]
     c = g.allreduce(_request(g, inputs, [(0, d, 0, 4, 128)], 12, True), nodes).outputs[0]
     assert (a == b).all() and not (a == c).all()
+
+
+@pytest.mark.parametrize("topology", ["ring", "tree"])
+def test_ring_and_tree_vs_compiled_reference(g, topology):
+    """run_ring / run_tree (collectives.cpp:312-471) on the GPU — every hop's
+    re-encode, the f32 folds in the reference's order, the owner/root's single
+    broadcast encode — against the compiled reference, bit for bit, with the
+    reference's byte, message, call, round and depth counters."""
+    from oracle import RefOracle
+    if not RefOracle.available():
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    ref = RefOracle()
+    rng = np.random.default_rng(23 if topology == "ring" else 29)
+    for trial in range(14):
+        nodes = [2, 3, 4, 5, 6, 7, 8][trial % 7]
+        d = int(rng.integers(1, 20000))
+        cuts = sorted(set(int(x) for x in rng.integers(1, max(2, d), int(rng.integers(0, 5)))))
+        edges = [0] + [x for x in cuts if 0 < x < d] + [d]
+        segs = []
+        for a, b in zip(edges[:-1], edges[1:]):
+            if rng.random() < 0.25:
+                segs.append((a, b - a, 2, 0, 0))
+            else:
+                segs.append((a, b - a, 0, int(rng.integers(1, 9)),
+                             int(rng.choice([1, 7, 32, 64, 128, 512, 1000]))))
+        inputs = [(rng.standard_normal(d) * 10.0 ** rng.integers(-3, 3)).astype(np.float32)
+                  for _ in range(nodes)]
+        step_seed = int(rng.integers(0, 2**63))
+        average = bool(rng.random() < 0.7)
+        want, sent, ctr = ref.allreduce(inputs, segs, step_seed, average, topology)
+        req = _request(g, inputs, segs, step_seed, average)
+        req.topology = getattr(g.Topology, topology)
+        res = g.allreduce(req, nodes)
+        for k, o in enumerate(res.outputs):
+            assert (o.view(np.uint32) == want[k].view(np.uint32)).all(), (trial, nodes, d, segs)
+        tr = res.trace
+        assert list(tr.bytes_sent) == sent, (trial, nodes, segs)
+        assert tr.compress_calls == ctr["compress_calls"], (trial, ctr)
+        assert tr.decompress_calls == ctr["decompress_calls"], (trial, ctr)
+        assert tr.message_count == ctr["message_count"] and tr.rounds == ctr["rounds"], ctr
+        assert tr.max_compress_depth == ctr["max_compress_depth"], (trial, ctr)
