@@ -163,6 +163,23 @@ int gcx_sra_reduce(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_
                    uint8_t* bcast, float* out, float divisor, const unsigned long long* keys,
                    unsigned long long* bad_key, void* stream);
 
+/* ---- exact wire framing (codec.cpp:216-259, collectives.cpp:143-194) ----
+ * The reference's message bytes for a piece table: per quantized piece the
+ * 17-byte LE header {u32 count, u8 bits, u32 bucket, u64 seed}, the f32
+ * norms and the ceil(len*(bits+1)/8) packed bytes; per raw piece its f32s.
+ * wire_layout (host): wire_off[k] per piece, returns the message length.
+ * frame: device message -> wire bytes (seed = the encode's seed, or the
+ *        pieces' own with GCX_F_PIECE_SEEDS).
+ * unframe: wire bytes -> device message; *err |= 1 when a header disagrees
+ *        with the layout (the reference's "chunk payload does not match piece
+ *        layout"); the caller checks the total length (trailing / short). */
+int64_t gcx_wire_layout(const gcx_piece* pieces, uint32_t npieces, uint64_t* wire_off);
+int gcx_frame_pieces(const gcx_piece* pieces, const uint64_t* wire_off, uint32_t npieces,
+                     const uint8_t* msg, uint64_t seed, uint32_t flags, uint8_t* wire,
+                     void* stream);
+int gcx_unframe_pieces(const gcx_piece* pieces, const uint64_t* wire_off, uint32_t npieces,
+                       const uint8_t* wire, uint8_t* msg, unsigned int* err, void* stream);
+
 /* acc[i] = acc[i] + x[i] in f32 (the ring and tree topologies' folds,
  * collectives.cpp:359-361 and :412-413). */
 int gcx_add_f32(float* acc, const float* x, uint64_t n, void* stream);

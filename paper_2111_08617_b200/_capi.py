@@ -87,6 +87,9 @@ _decl("gcx_sra_reduce", i32, vp, vp, u32, u32, u32, vp, u64, vp, u32, u32, u64, 
 _decl("gcx_hash_bench", i32, u64, u64, u32, i32, vp, vp)
 _decl("gcx_stats_accumulate", i32, vp, vp, u64, vp, vp)
 _decl("gcx_add_f32", i32, vp, vp, u64, vp)
+_decl("gcx_wire_layout", i64, C.POINTER(Piece), u32, C.POINTER(u64))
+_decl("gcx_frame_pieces", i32, vp, vp, u32, vp, u64, u32, vp, vp)
+_decl("gcx_unframe_pieces", i32, vp, vp, u32, vp, vp, vp, vp)
 _decl("gcx_device_info", i32, i32, C.POINTER(i32), C.POINTER(i32))
 
 EXPORTS = ["gcx_version", "gcx_last_error", "gcx_compressed_size", "gcx_packed_bytes",
@@ -95,7 +98,8 @@ EXPORTS = ["gcx_version", "gcx_last_error", "gcx_compressed_size", "gcx_packed_b
            "gcx_sra_reduce", "gcx_hash_bench", "gcx_device_info", "gcx_plan_keys",
            "gcx_make_keys", "gcx_fold_pieces", "gcx_prefix_slots", "gcx_make_prefix",
            "gcx_quantize_prefixed", "gcx_make_key_prefix", "gcx_make_keys_prefixed",
-           "gcx_stats_accumulate", "gcx_add_f32"]
+           "gcx_stats_accumulate", "gcx_add_f32", "gcx_wire_layout", "gcx_frame_pieces",
+           "gcx_unframe_pieces"]
 
 
 def lib():

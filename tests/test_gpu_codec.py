@@ -286,3 +286,79 @@ def test_prefixed_quantize_matches_oracle(dev, oracle, bits, bucket, n, zeros):
         wn, wp = oracle.quantize(v, bits, bucket, seed)
         assert (norms.cpu().numpy().view(np.uint32) == wn.view(np.uint32)).all()
         assert (packed.cpu().numpy()[: wp.size] == wp).all()
+
+
+def test_wire_framing_is_the_reference_message(dev, oracle):
+    """gcx_frame_pieces turns a device message into the reference's exact
+    encode_pieces bytes (collectives.cpp:143-163: serialize() per quantized
+    piece -- 17-byte header, norms, packed -- raw f32 otherwise), and
+    gcx_unframe_pieces restores the device message; a header that disagrees
+    with the layout is flagged."""
+    import ctypes as C
+    from paper_2111_08617_b200 import _capi
+    rng = np.random.default_rng(31)
+    lens = [int(x) for x in rng.integers(1, 7000, 17)] + [1, 4096, 4097]
+    pieces, off, src_off = [], 0, 0
+    for k, n in enumerate(lens):
+        bits = int(rng.integers(1, 9)) if k % 4 else 0
+        bucket = int(rng.choice([7, 64, 128, 1000])) if bits else 0
+        if bits:
+            nb = (n + bucket - 1) // bucket
+            norms_off = off
+            packed_off = (off + 4 * nb + 15) // 16 * 16
+            off = (packed_off + _capi.packed_capacity(n, bits) + 15) // 16 * 16
+        else:
+            norms_off = packed_off = off
+            off = (off + 4 * n + 15) // 16 * 16
+        pieces.append(_capi.Piece(src_off, n, norms_off, packed_off, 0, bucket, bits))
+        src_off += n
+    x = (rng.standard_normal(src_off) * 0.1).astype(np.float32)
+    seed = 0x5151_0001
+    arr = (_capi.Piece * len(pieces))(*pieces)
+    nt, prefix, flags = _capi.plan_tiles(list(arr))
+    wire_off = (C.c_uint64 * len(pieces))()
+    total = _capi.lib().gcx_wire_layout(arr, len(pieces), wire_off)
+    dev_pieces = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).cuda()
+    dev_prefix = torch.tensor(prefix, dtype=torch.int32).cuda()
+    dev_woff = torch.tensor(list(wire_off), dtype=torch.int64).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    msg = torch.zeros(off + 64, dtype=torch.uint8, device="cuda")
+    bad = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    xd = torch.from_numpy(x).cuda()
+    _capi.check(_capi.lib().gcx_encode_pieces(dev_pieces.data_ptr(), dev_prefix.data_ptr(),
+                                              len(pieces), nt, flags, seed, xd.data_ptr(),
+                                              msg.data_ptr(), None, bad.data_ptr(), st))
+    wire = torch.zeros(total, dtype=torch.uint8, device="cuda")
+    _capi.check(_capi.lib().gcx_frame_pieces(dev_pieces.data_ptr(), dev_woff.data_ptr(),
+                                             len(pieces), msg.data_ptr(), seed, 0,
+                                             wire.data_ptr(), st))
+    torch.cuda.synchronize()
+    want = []
+    for p in pieces:
+        part = x[p.src:p.src + p.len]
+        if p.bits == 0:
+            want.append(part.view(np.uint8))
+        else:
+            wn, wp = oracle.quantize(part, p.bits, p.bucket, seed)
+            want.append(oracle.serialize(wn, wp, p.len, p.bits, p.bucket, seed))
+    want = np.concatenate(want)
+    assert want.size == total
+    assert (wire.cpu().numpy() == want).all()
+    # back to the device layout
+    msg2 = torch.zeros_like(msg)
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _capi.check(_capi.lib().gcx_unframe_pieces(dev_pieces.data_ptr(), dev_woff.data_ptr(),
+                                               len(pieces), wire.data_ptr(), msg2.data_ptr(),
+                                               err.data_ptr(), st))
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    assert torch.equal(msg, msg2)
+    # a header whose element count disagrees with the layout is flagged
+    k = next(i for i, p in enumerate(pieces) if p.bits)
+    bad_wire = wire.clone()
+    bad_wire[wire_off[k]] ^= 1
+    _capi.check(_capi.lib().gcx_unframe_pieces(dev_pieces.data_ptr(), dev_woff.data_ptr(),
+                                               len(pieces), bad_wire.data_ptr(), msg2.data_ptr(),
+                                               err.data_ptr(), st))
+    torch.cuda.synchronize()
+    assert int(err.item()) == 1
