@@ -183,6 +183,8 @@ int gcx_unframe_pieces(const gcx_piece* pieces, const uint64_t* wire_off, uint32
 /* acc[i] = acc[i] + x[i] in f32 (the ring and tree topologies' folds,
  * collectives.cpp:359-361 and :412-413). */
 int gcx_add_f32(float* acc, const float* x, uint64_t n, void* stream);
+/* x[i] = x[i] / divisor (IEEE f32; finalize's average). */
+int gcx_div_f32(float* x, uint64_t n, float divisor, void* stream);
 
 /* ---- microbenchmarks ----
  * Integer ceiling of the reference RNG: n draws of uniform01(seed, i/bucket, i),
@@ -209,6 +211,19 @@ int gcx_sq_error(const float* a, const float* b, uint64_t n, double* scratch, do
  * observation feed, engine.cpp:268-283); stack = nodes rows of n floats */
 int gcx_mean_nodes(const float* stack, uint32_t nodes, uint64_t n, float* out, void* stream);
 const char* gcx_stats_last_error(void);
+
+/* ---- TopK + error feedback, the reference's sparse codec (codec.cpp:158-214) ----
+ * compress: residual <- v + residual; idx_out[0..k) = the k largest |acc|
+ *           (ties to the lower index) in increasing order, val_out = their
+ *           acc values, residual[idx] = 0.  *bad = min non-finite index of v
+ *           (preset to UINT64_MAX).  scratch >= gcx_topk_scratch_bytes(n).
+ * densify:  dense = 0, dense[idx[j]] = val[j]  (topk_decompress). */
+uint64_t gcx_topk_scratch_bytes(uint64_t n);
+int gcx_topk_compress(const float* v, uint64_t n, uint64_t k, float* residual, uint32_t* idx_out,
+                      float* val_out, void* scratch, uint64_t scratch_bytes,
+                      unsigned long long* bad, void* stream);
+int gcx_topk_densify(const uint32_t* idx, const float* val, uint64_t k, uint64_t n, float* dense,
+                     void* stream);
 
 /* Number of SMs and the kernels' resident CTAs per SM (device 0..). */
 int gcx_device_info(int device, int* sms, int* encode_ctas_per_sm);

@@ -252,6 +252,13 @@ class RefOracle:
         L.ref_allreduce.argtypes = [C.POINTER(C.POINTER(flt)), u64, u64, C.POINTER(Segment), u64,
                                     u64, C.c_int, C.POINTER(C.POINTER(flt)), C.POINTER(u64),
                                     C.POINTER(u64)]
+        L.ref_topk_compress.restype = C.c_int
+        L.ref_topk_compress.argtypes = [C.POINTER(flt), u64, u64, C.POINTER(flt), C.POINTER(u64),
+                                        C.POINTER(flt)]
+        L.ref_sparse_allreduce.restype = C.c_int
+        L.ref_sparse_allreduce.argtypes = [u64, u64, C.POINTER(u64), C.POINTER(C.POINTER(u64)),
+                                           C.POINTER(C.POINTER(flt)), C.c_int,
+                                           C.POINTER(C.POINTER(flt)), C.POINTER(u64)]
         L.ref_hop_seed.restype = u64
         L.ref_hop_seed.argtypes = [u64, u64, u64]
         L.ref_engine_run.restype = C.c_int
@@ -300,6 +307,30 @@ class RefOracle:
         keys = ["compress_calls", "decompress_calls", "message_count", "rounds",
                 "max_compress_depth"]
         return outs, list(sent), dict(zip(keys, list(ctr)))
+
+    def topk_compress(self, v, k, residual):
+        """-> (indices u64[k], values f32[k], new residual); codec.cpp:158-193."""
+        v = np.ascontiguousarray(v, np.float32)
+        r = np.array(residual, np.float32, copy=True)
+        idx = np.zeros(max(k, 1), np.uint64)
+        val = np.zeros(max(k, 1), np.float32)
+        self._check(self.lib.ref_topk_compress(_f32p(v), v.size, k, _f32p(r),
+                                               idx.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                               _f32p(val)))
+        return idx[:k], val[:k], r
+
+    def sparse_allreduce(self, chunks, d, average=True):
+        """chunks: [(indices, values)] per node -> (outputs, bytes_sent)."""
+        nodes = len(chunks)
+        ids = [np.ascontiguousarray(c[0], np.uint64) for c in chunks]
+        vals = [np.ascontiguousarray(c[1], np.float32) for c in chunks]
+        ks = (C.c_uint64 * nodes)(*[len(i) for i in ids])
+        ip = (C.POINTER(C.c_uint64) * nodes)(*[i.ctypes.data_as(C.POINTER(C.c_uint64)) for i in ids])
+        outs = [np.empty(d, np.float32) for _ in range(nodes)]
+        sent = (C.c_uint64 * nodes)()
+        self._check(self.lib.ref_sparse_allreduce(nodes, d, ks, ip, _ptrs(vals),
+                                                  1 if average else 0, _ptrs(outs), sent))
+        return outs, list(sent)
 
     def engine_run(self, nodes, layers, steps, tag, plan_json=None, adaptive_json=None,
                    step_seed=1, fuse_limit=0):

@@ -139,6 +139,53 @@ int ref_allreduce_topo(const float* const* inputs, std::uint64_t nodes, std::uin
   }
 }
 
+// codec::topk_compress (codec.cpp:158-193); residual is updated in place
+int ref_topk_compress(const float* v, std::uint64_t n, std::uint64_t k, float* residual,
+                      std::uint64_t* idx_out, float* val_out) {
+  try {
+    gcomm::codec::ErrorFeedbackState st;
+    st.residual.assign(residual, residual + n);
+    auto c = gcomm::codec::topk_compress(std::span<const float>(v, n), k, st);
+    for (std::size_t i = 0; i < c.k; ++i) {
+      idx_out[i] = c.indices[i];
+      val_out[i] = c.values[i];
+    }
+    std::memcpy(residual, st.residual.data(), 4 * n);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// collectives::sparse_allreduce over SimNet (collectives.cpp:533-603)
+int ref_sparse_allreduce(std::uint64_t nodes, std::uint64_t d, const std::uint64_t* ks,
+                         const std::uint64_t* const* idx, const float* const* vals, int op,
+                         float* const* outputs, std::uint64_t* bytes_sent) {
+  try {
+    std::vector<gcomm::codec::SparseChunk> chunks(nodes);
+    for (std::uint64_t r = 0; r < nodes; ++r) {
+      chunks[r].original_length = d;
+      chunks[r].k = ks[r];
+      chunks[r].indices.assign(idx[r], idx[r] + ks[r]);
+      chunks[r].values.assign(vals[r], vals[r] + ks[r]);
+    }
+    gcomm::simnet::SimNetConfig cfg;
+    cfg.nodes = nodes;
+    gcomm::simnet::SimNet net(cfg);
+    auto res = gcomm::collectives::sparse_allreduce(
+        chunks, op ? gcomm::collectives::ReduceOp::average : gcomm::collectives::ReduceOp::sum, net);
+    for (std::uint64_t r = 0; r < nodes; ++r) {
+      std::memcpy(outputs[r], res.outputs[r].data(), 4 * d);
+      if (bytes_sent) bytes_sent[r] = res.trace.bytes_sent[r];
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 std::uint64_t ref_hop_seed(std::uint64_t s, std::uint64_t hop, std::uint64_t node) {
   return gcomm::collectives::hop_seed(s, hop, node);
 }

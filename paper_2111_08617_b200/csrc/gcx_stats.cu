@@ -152,9 +152,111 @@ uint32_t grid(uint64_t n) {
   return uint32_t(g < 4096 ? (g ? g : 1) : 4096);
 }
 
+// ---------------------------------------------------------------------------
+// TopK + error feedback (codec.cpp:158-214): acc = v + residual; keep the k
+// largest |acc| (ties to the lower index) in increasing index order; residual
+// = acc with the kept entries zeroed.  The selection order is a total order on
+// the 64-bit key (|acc| bits << 32) | (2^32 - 1 - i): |acc| as unsigned bits
+// is monotone for non-negative floats, and the complemented index makes the
+// lower index win a tie; a descending radix sort of the keys gives exactly the
+// reference's nth_element partition.
+// ---------------------------------------------------------------------------
+__global__ void k_topk_acc(const float* __restrict__ v, float* __restrict__ residual, uint64_t n,
+                           unsigned long long* __restrict__ keys,
+                           unsigned long long* __restrict__ bad) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const float x = v[i];
+    if (!isfinite(x)) atomicMin(bad, (unsigned long long)i);
+    const float a = __fadd_rn(x, residual[i]);
+    residual[i] = a;
+    const uint32_t mag = __float_as_uint(a) & 0x7FFFFFFFu;
+    keys[i] = (unsigned long long)mag << 32 | (0xFFFFFFFFu - uint32_t(i));
+  }
+}
+
+// the k winners' indices (from the sorted keys), for the index sort
+__global__ void k_topk_idx(const unsigned long long* __restrict__ sorted, uint64_t k,
+                           uint32_t* __restrict__ idx) {
+  for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < k;
+       j += uint64_t(gridDim.x) * blockDim.x)
+    idx[j] = 0xFFFFFFFFu - uint32_t(sorted[j]);
+}
+
+__global__ void k_topk_take(const uint32_t* __restrict__ idx, uint64_t k, float* __restrict__ residual,
+                            float* __restrict__ val) {
+  for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < k;
+       j += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t i = idx[j];
+    val[j] = residual[i];
+    residual[i] = 0.0f;
+  }
+}
+
+// dense[i] = 0, then dense[idx[j]] = val[j] (topk_decompress)
+__global__ void k_zero(float* __restrict__ x, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    x[i] = 0.0f;
+}
+
+__global__ void k_scatter(const uint32_t* __restrict__ idx, const float* __restrict__ val,
+                          uint64_t k, float* __restrict__ dense) {
+  for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < k;
+       j += uint64_t(gridDim.x) * blockDim.x)
+    dense[idx[j]] = val[j];
+}
+
 }  // namespace
 
 extern "C" {
+
+uint64_t gcx_topk_scratch_bytes(uint64_t n) {
+  size_t t1 = 0, t2 = 0;
+  const int m = int(n > 0 ? n : 1);
+  cub::DeviceRadixSort::SortKeysDescending(nullptr, t1, (unsigned long long*)nullptr,
+                                           (unsigned long long*)nullptr, m);
+  cub::DeviceRadixSort::SortKeys(nullptr, t2, (uint32_t*)nullptr, (uint32_t*)nullptr, m);
+  return 2 * 8 * n + 2 * 4 * n + (t1 > t2 ? t1 : t2) + 512;
+}
+
+int gcx_topk_compress(const float* v, uint64_t n, uint64_t k, float* residual, uint32_t* idx_out,
+                      float* val_out, void* scratch, uint64_t scratch_bytes,
+                      unsigned long long* bad, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (k < 1 || k > n) {
+    g_err2 = "topk k must be in [1, length], got " + std::to_string(k);
+    return GCX_E_INVALID;
+  }
+  if (n >= (1ull << 31)) {
+    g_err2 = "gcx_topk_compress: length must be below 2^31";
+    return GCX_E_INVALID;
+  }
+  if (scratch_bytes < gcx_topk_scratch_bytes(n)) {
+    g_err2 = "gcx_topk_compress: scratch too small";
+    return GCX_E_INVALID;
+  }
+  auto* keys = static_cast<unsigned long long*>(scratch);
+  auto* sorted = keys + n;
+  auto* idx = reinterpret_cast<uint32_t*>(sorted + n);
+  const uintptr_t t0 = (reinterpret_cast<uintptr_t>(idx + 2 * n) + 255) & ~uintptr_t(255);
+  void* temp = reinterpret_cast<void*>(t0);
+  size_t temp_bytes = scratch_bytes - (t0 - reinterpret_cast<uintptr_t>(scratch));
+  k_topk_acc<<<grid(n), kThreads, 0, st>>>(v, residual, n, keys, bad);
+  cub::DeviceRadixSort::SortKeysDescending(temp, temp_bytes, keys, sorted, int(n), 0, 64, st);
+  k_topk_idx<<<grid(k), kThreads, 0, st>>>(sorted, k, idx);
+  cub::DeviceRadixSort::SortKeys(temp, temp_bytes, idx, idx_out, int(k), 0, 32, st);
+  k_topk_take<<<grid(k), kThreads, 0, st>>>(idx_out, k, residual, val_out);
+  return launch_check("gcx_topk_compress");
+}
+
+int gcx_topk_densify(const uint32_t* idx, const float* val, uint64_t k, uint64_t n, float* dense,
+                     void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n) k_zero<<<grid(n), kThreads, 0, st>>>(dense, n);
+  if (k) k_scatter<<<grid(k), kThreads, 0, st>>>(idx, val, k, dense);
+  return launch_check("gcx_topk_densify");
+}
 
 const char* gcx_stats_last_error(void) { return g_err2.c_str(); }
 

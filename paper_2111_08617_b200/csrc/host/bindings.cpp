@@ -89,6 +89,33 @@ PYBIND11_MODULE(_gcomm, m) {
     return codec::quantize(std::span<const float>(v.data(), std::size_t(v.size())), p);
   });
   m.def("dequantize", [](const codec::CompressedChunk& c) { return to_np(codec::dequantize(c)); });
+
+  py::class_<codec::SparseChunk>(m, "SparseChunk")
+      .def(py::init<>())
+      .def_readwrite("original_length", &codec::SparseChunk::original_length)
+      .def_readwrite("k", &codec::SparseChunk::k)
+      .def_property(
+          "indices",
+          [](const codec::SparseChunk& c) {
+            std::vector<std::uint64_t> v(c.indices.begin(), c.indices.end());
+            return to_np(v);
+          },
+          [](codec::SparseChunk& c, py::array_t<std::uint64_t, py::array::c_style | py::array::forcecast> a) {
+            c.indices.assign(a.data(), a.data() + a.size());
+          })
+      .def_property(
+          "values", [](const codec::SparseChunk& c) { return to_np(c.values); },
+          [](codec::SparseChunk& c, farr a) { c.values = from_np<float>(a); });
+  py::class_<codec::ErrorFeedbackState>(m, "ErrorFeedbackState")
+      .def(py::init<>())
+      .def(py::init<std::size_t>())
+      .def_property(
+          "residual", [](const codec::ErrorFeedbackState& e) { return to_np(e.residual); },
+          [](codec::ErrorFeedbackState& e, farr a) { e.residual = from_np<float>(a); });
+  m.def("topk_compress", [](farr v, std::size_t k, codec::ErrorFeedbackState& state) {
+    return codec::topk_compress(std::span<const float>(v.data(), std::size_t(v.size())), k, state);
+  });
+  m.def("topk_decompress", [](const codec::SparseChunk& c) { return to_np(codec::topk_decompress(c)); });
   m.def("pack_levels", [](u32arr levels, u8arr signs, int bits) {
     return to_np(codec::pack_levels(std::span<const std::uint32_t>(levels.data(), levels.size()),
                                     std::span<const std::uint8_t>(signs.data(), signs.size()), bits));
@@ -256,6 +283,8 @@ PYBIND11_MODULE(_gcomm, m) {
   });
   m.def("allreduce", &collectives::allreduce, py::arg("request"), py::arg("nodes"),
         py::call_guard<py::gil_scoped_release>());
+  m.def("sparse_allreduce", &collectives::sparse_allreduce, py::arg("chunks"), py::arg("op"),
+        py::arg("nodes"), py::call_guard<py::gil_scoped_release>());
 
   py::class_<collectives::Communicator>(m, "Communicator")
       .def(py::init([](int rank, int nranks, py::bytes id) {

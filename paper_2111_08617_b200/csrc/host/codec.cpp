@@ -146,6 +146,84 @@ std::vector<float> dequantize(const CompressedChunk& chunk) {
   return out;
 }
 
+// codec.cpp:158-193 on the GPU (gcx_topk_compress): accumulate, select by
+// (|acc| desc, index asc), sort the winners' indices, zero them in the residual
+SparseChunk topk_compress(std::span<const float> values, std::size_t k, ErrorFeedbackState& state) {
+  const std::size_t n = values.size();
+  if (k < 1 || k > n)
+    throw std::invalid_argument("topk k must be in [1, length], got " + std::to_string(k));
+  if (state.residual.size() != n)
+    throw std::invalid_argument("error feedback state length does not match input");
+  Scratch& s = scratch();
+  cudaStream_t st = s.stream.get();
+  s.x.ensure(4 * n);
+  s.out.ensure(4 * n);  // residual / accumulator
+  s.norms.ensure(4 * k);  // values
+  s.packed.ensure(4 * k);  // indices
+  s.bad.ensure(8);
+  static thread_local DeviceBuffer work;
+  const std::uint64_t wb = gcx_topk_scratch_bytes(n);
+  work.ensure(wb);
+  cuda_check(cudaMemcpyAsync(s.x.get(), values.data(), 4 * n, cudaMemcpyHostToDevice, st), "H2D");
+  cuda_check(cudaMemcpyAsync(s.out.get(), state.residual.data(), 4 * n, cudaMemcpyHostToDevice, st),
+             "H2D");
+  cuda_check(cudaMemsetAsync(s.bad.get(), 0xFF, 8, st), "memset");
+  const int rc = gcx_topk_compress(s.x.get<float>(), n, k, s.out.get<float>(),
+                                   s.packed.get<std::uint32_t>(), s.norms.get<float>(), work.get(), wb,
+                                   s.bad.get<unsigned long long>(), st);
+  if (rc == GCX_E_INVALID) throw std::invalid_argument(gcx_stats_last_error());
+  if (rc != GCX_OK) throw std::runtime_error(gcx_stats_last_error());
+  std::uint64_t bad = 0;
+  std::vector<std::uint32_t> idx(k);
+  SparseChunk chunk;
+  chunk.original_length = n;
+  chunk.k = k;
+  chunk.values.resize(k);
+  std::vector<float> residual(n);
+  cuda_check(cudaMemcpyAsync(&bad, s.bad.get(), 8, cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaMemcpyAsync(idx.data(), s.packed.get(), 4 * k, cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaMemcpyAsync(chunk.values.data(), s.norms.get(), 4 * k, cudaMemcpyDeviceToHost, st),
+             "D2H");
+  cuda_check(cudaMemcpyAsync(residual.data(), s.out.get(), 4 * n, cudaMemcpyDeviceToHost, st), "D2H");
+  s.stream.sync();
+  if (bad != ~0ULL)  // codec.cpp:170-172 (the state is left untouched)
+    throw std::invalid_argument("non-finite gradient value at index " + std::to_string(bad));
+  chunk.indices.assign(idx.begin(), idx.end());
+  state.residual = std::move(residual);
+  return chunk;
+}
+
+// codec.cpp:195-209: validation on the host, the scatter on the GPU
+std::vector<float> topk_decompress(const SparseChunk& chunk) {
+  if (chunk.indices.size() != chunk.values.size() || chunk.indices.size() != chunk.k)
+    throw std::runtime_error("sparse chunk index/value arity mismatch");
+  for (std::size_t i = 0; i < chunk.k; ++i) {
+    if (chunk.indices[i] >= chunk.original_length)
+      throw std::runtime_error("sparse index out of range");
+    if (i > 0 && chunk.indices[i] <= chunk.indices[i - 1])
+      throw std::runtime_error("sparse indices must be strictly increasing");
+  }
+  const std::size_t n = chunk.original_length, k = chunk.k;
+  std::vector<float> out(n);
+  if (n == 0) return out;
+  Scratch& s = scratch();
+  cudaStream_t st = s.stream.get();
+  s.out.ensure(4 * n);
+  s.norms.ensure(4 * k + 4);
+  s.packed.ensure(4 * k + 4);
+  std::vector<std::uint32_t> idx(chunk.indices.begin(), chunk.indices.end());
+  if (k) {
+    cuda_check(cudaMemcpyAsync(s.packed.get(), idx.data(), 4 * k, cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(s.norms.get(), chunk.values.data(), 4 * k, cudaMemcpyHostToDevice, st),
+               "H2D");
+  }
+  gcx_check(gcx_topk_densify(s.packed.get<std::uint32_t>(), s.norms.get<float>(), k, n,
+                             s.out.get<float>(), st));
+  cuda_check(cudaMemcpyAsync(out.data(), s.out.get(), 4 * n, cudaMemcpyDeviceToHost, st), "D2H");
+  s.stream.sync();
+  return out;
+}
+
 // Byte-format utilities (codec.cpp:97-149): the field layout of the packed
 // stream, exposed so the packing identity can be checked without the GPU.
 std::vector<std::uint8_t> pack_levels(std::span<const std::uint32_t> levels,

@@ -593,6 +593,72 @@ ReduceResult allreduce_tree(const ReduceRequest& req, std::size_t N) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
+// sparse path (collectives.cpp:533-603), all nodes on one GPU
+// ---------------------------------------------------------------------------
+ReduceResult sparse_allreduce(const std::vector<codec::SparseChunk>& chunks, ReduceOp op,
+                              std::size_t nodes) {
+  if (chunks.size() != nodes) throw std::invalid_argument("expected one sparse chunk per node");
+  const std::size_t d = chunks.empty() ? 0 : chunks[0].original_length;
+  for (const auto& c : chunks)
+    if (c.original_length != d)
+      throw std::invalid_argument("sparse chunks disagree on vector length");
+  ReduceResult result;
+  if (nodes == 1) {
+    result.outputs.assign(1, codec::topk_decompress(chunks[0]));
+    result.trace.bytes_sent.assign(1, 0);
+    result.trace.bytes_received.assign(1, 0);
+    return result;
+  }
+  for (const auto& c : chunks) {  // parse_sparse / topk_decompress validation
+    if (c.indices.size() != c.values.size() || c.indices.size() != c.k)
+      throw std::runtime_error("sparse chunk index/value arity mismatch");
+    for (std::size_t i = 0; i < c.k; ++i) {
+      if (c.indices[i] >= d) throw std::runtime_error("sparse index out of range");
+      if (i > 0 && c.indices[i] <= c.indices[i - 1])
+        throw std::runtime_error("sparse indices must be strictly increasing");
+    }
+  }
+  detail::require_device();
+  detail::Stream stream;
+  cudaStream_t st = stream.get();
+  std::size_t kmax = 1;
+  for (const auto& c : chunks) kmax = std::max(kmax, c.k);
+  DeviceBuffer out(4 * d + 16), dense(4 * d + 16), idx(4 * kmax + 16), val(4 * kmax + 16);
+  cuda_check(cudaMemsetAsync(out.get(), 0, 4 * d, st), "memset");
+  std::vector<std::uint32_t> hidx;
+  for (std::size_t id = 0; id < nodes; ++id) {  // out[i] += dense_id[i], ascending id
+    const auto& c = chunks[id];
+    hidx.assign(c.indices.begin(), c.indices.end());
+    if (c.k) {
+      cuda_check(cudaMemcpyAsync(idx.get(), hidx.data(), 4 * c.k, cudaMemcpyHostToDevice, st), "H2D");
+      cuda_check(cudaMemcpyAsync(val.get(), c.values.data(), 4 * c.k, cudaMemcpyHostToDevice, st),
+                 "H2D");
+    }
+    gcx_check(gcx_topk_densify(idx.get<std::uint32_t>(), val.get<float>(), c.k, d,
+                               dense.get<float>(), st));
+    gcx_check(gcx_add_f32(out.get<float>(), dense.get<float>(), d, st));
+    stream.sync();  // hidx is reused
+  }
+  if (op == ReduceOp::average) gcx_check(gcx_div_f32(out.get<float>(), d, float(nodes), st));
+  std::vector<float> host(d);
+  cuda_check(cudaMemcpyAsync(host.data(), out.get(), 4 * d, cudaMemcpyDeviceToHost, st), "D2H");
+  stream.sync();
+  result.outputs.assign(nodes, host);  // every node sums the same chunks in the same order
+  StepTrace& tr = result.trace;
+  tr.bytes_sent.assign(nodes, 0);
+  tr.bytes_received.assign(nodes, 0);
+  for (std::size_t me = 0; me < nodes; ++me) {
+    const std::uint64_t b = 8 + 8 * chunks[me].k;  // serialize_sparse
+    tr.bytes_sent[me] = (nodes - 1) * b;
+    for (std::size_t r = 0; r < nodes; ++r)
+      if (r != me) tr.bytes_received[r] += b;
+  }
+  tr.message_count = nodes * (nodes - 1);
+  tr.rounds = 1;
+  return result;
+}
+
+// ---------------------------------------------------------------------------
 // all nodes on one GPU
 // ---------------------------------------------------------------------------
 ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {

@@ -56,6 +56,23 @@ std::vector<std::uint8_t> serialize(const CompressedChunk& chunk);
 CompressedChunk parse_chunk(std::span<const std::uint8_t> bytes);
 std::size_t serialized_size_bytes(std::size_t element_count, const QuantParams& params);
 
+// include/gcomm/codec.hpp:28-42, 59-61: TopK selection with error feedback
+struct SparseChunk {
+  std::size_t original_length = 0;
+  std::size_t k = 0;
+  std::vector<std::size_t> indices;
+  std::vector<float> values;
+};
+
+struct ErrorFeedbackState {
+  std::vector<float> residual;
+  ErrorFeedbackState() = default;
+  explicit ErrorFeedbackState(std::size_t length) : residual(length, 0.0f) {}
+};
+
+SparseChunk topk_compress(std::span<const float> values, std::size_t k, ErrorFeedbackState& state);
+std::vector<float> topk_decompress(const SparseChunk& chunk);
+
 }  // namespace codec
 
 namespace model {
@@ -199,6 +216,12 @@ StepTrace sra_trace(const SraLayout& layout);
 // all `nodes` run on the current GPU (one process), the exchange is
 // device-local.  Outputs are bit-identical to the reference's.
 ReduceResult allreduce(const ReduceRequest& request, std::size_t nodes);
+
+// Drop-in for collectives::sparse_allreduce(chunks, op, SimNet&)
+// (collectives.cpp:533-603): every node's sparse chunk is densified and the
+// dense vectors summed in ascending node order on this GPU (÷N for average).
+ReduceResult sparse_allreduce(const std::vector<codec::SparseChunk>& chunks, ReduceOp op,
+                              std::size_t nodes);
 
 // ---------------- one process per GPU (NCCL over NVLink) ----------------
 class Communicator {
