@@ -200,3 +200,20 @@ def test_stats_collector_window_sums(g, oracle):
     with pytest.raises(ValueError, match="fed twice"):
         col.add("w", a)
         col.add("w", a)
+
+
+@pytest.mark.parametrize("nodes", [2, 3, 4])
+def test_engine_topk_layers_match_reference(g, oracle, nodes):
+    """engine.cpp:191-266: topk layers leave the fused buffers, keep a
+    per-node error-feedback residual across steps and reduce through the
+    sparse path; the rest of the step is unchanged."""
+    if not RefOracle.available():
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    layers = [("conv1.w", 9408, 0, 0.001), ("bn1.w", 64, 2, 0.01), ("emb.w", 30000, 3, 0.02),
+              ("layer1.conv.w", 36864, 0, 0.001), ("fc.w", 20480, 0, 0.01), ("fc.b", 10, 1, 0.01)]
+    plan = json.dumps({"defaults": {"bits": 4, "bucket": 128},
+                       "layers": {"emb.w": {"mode": "topk", "k": 1500},
+                                  "fc.w": {"mode": "topk", "k": 64}}})
+    got, _ = run_engine(g, oracle, nodes, layers, 4, 0x7A, plan)
+    want, _ = RefOracle().engine_run(nodes, layers, 4, 0x7A, plan)
+    assert got == want
