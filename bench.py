@@ -301,6 +301,11 @@ def run_codec(args):
     acc_ms = a0.elapsed_time(a1) / args.steps
     del wsum
 
+    # the N = 8 SRA step of the ResNet-50 layer list with every rank's kernels
+    # on this GPU (exchange in device memory): per-rank kernel time, the
+    # compute side of the multi-GPU number (scripts/sra_emul_bench.py)
+    sra8 = sra_emulation(8)
+
     # end to end through the C-ABI with host buffers: every step copies its
     # input from pinned host memory (H2D), runs gcx_quantize + gcx_dequantize
     # and reads the result back (D2H).  Steps are double-buffered over three
@@ -335,6 +340,7 @@ def run_codec(args):
                            "once per buffer shape (gcx_make_prefix, outside the timed region); "
                            "each step hashes mix64(seed ^ T(i)) with a fresh seed",
                    "quantize_inline_ms": q_inline_ms,
+                   "sra_n8_emulated_per_rank_kernel_ms": sra8,
                    "k4_window_accumulate_ms": acc_ms,
                    "k4_window_accumulate_GBps": 20 * n / (acc_ms * 1e-3) / 1e9,
                    "k4_note": "adaptive statistics: sum[i] += (double)g[i] (read 4+8 B, write 8 B "
@@ -359,6 +365,33 @@ def run_codec(args):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def sra_emulation(nodes):
+    """Kernel time per rank of one SRA step (ResNet-50 layer list, default
+    filter, 4b/128, 64 MiB buffers, average) with all `nodes` ranks' K1 /
+    fold / K3 run on this GPU; best of 3 after a warm-up."""
+    import numpy as np
+
+    from paper_2111_08617_b200 import _gcomm as G
+    from paper_2111_08617_b200.ddp import load_layout, resolve_codecs
+    layers = load_layout("resnet50")
+    codecs = resolve_codecs(layers)
+    total = 0.0
+    rng = np.random.default_rng(0)
+    for fb in G.pack_fused_buffers([n for _, n, _ in layers], 64 << 20):
+        segs = [G.Segment(s.buffer_offset, s.length, codecs[s.tensor_index].mode,
+                          codecs[s.tensor_index].bits, codecs[s.tensor_index].bucket_size)
+                for s in fb.segments]
+        req = G.ReduceRequest()
+        req.inputs = [(rng.standard_normal(fb.total_elements) * 1e-3).astype(np.float32)
+                      for _ in range(nodes)]
+        req.segments = segs
+        req.op = G.ReduceOp.average
+        req.step_seed = 7
+        G.allreduce(req, nodes)
+        total += min(G.allreduce(req, nodes).trace.device_time_s for _ in range(3))
+    return total * 1e3 / nodes
 
 
 def e2e_codec(args, sets, n, bits, bucket):
