@@ -353,8 +353,10 @@ def run_codec(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_quant32 (K1: fused bucket norms + stochastic quantize + pack, "
                                "one launch per gcx_quantize)", "peak_kind": peak_kind,
-                     "note": "K1 is integer-ALU bound by the reference RNG (3 SplitMix64 "
-                             "finalizers per element); config.hash_only_ms is its ceiling",
+                     "note": "K1 is integer-bound by the reference RNG; with the key prefixes "
+                             "it hashes one SplitMix64 finalizer per element and reads the "
+                             "8-byte prefix T(i) (traffic ~ 4+8 B/elem vs 4.6 algorithmic); "
+                             "config.hash_only_ms is the three-finalizer hash alone",
                      "algorithmic_bytes_per_launch": q_bytes},
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": 4 * n / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
