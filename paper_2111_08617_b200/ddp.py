@@ -114,3 +114,66 @@ def make_communicator(rank: int, world: int):
     if world > 1:
         dist.broadcast_object_list(uid, src=0)
     return G.Communicator(rank, world, uid[0])
+
+
+class CgxCommHook:
+    """PyTorch DDP communication hook: each gradient bucket DDP hands over is
+    averaged across ranks by the compressed SRA allreduce, in place.
+
+    ``model.register_comm_hook(CgxCommHook(comm), cgx_comm_hook)``.  The bucket's
+    flat buffer holds its parameters' gradients back to back; each parameter
+    is a layer with the reference's filter rules and plan (engine.cpp:178-190):
+    1-D parameters count as bias / norm and stay uncompressed by the default
+    filter, as do layers under 4096 elements.  One DeviceReducer per bucket
+    index is built on first use (DDP keeps bucket layouts fixed after the
+    first iteration); the per-bucket step seed follows engine.cpp:208-209
+    with the bucket index in place of the fused-buffer index.
+    """
+
+    def __init__(self, comm, plan=None, filters=None, step_seed=1):
+        self.comm = comm
+        self.plan = plan
+        self.filters = filters
+        self.step_seed = step_seed
+        self.step = 0
+        self.calls = 0
+        self._reducers = {}
+
+    def _reducer(self, bucket):
+        idx = bucket.index()
+        red = self._reducers.get(idx)
+        if red is None:
+            layers = []
+            for k, p in enumerate(bucket.parameters()):
+                kind = "weight" if p.dim() > 1 else "bias"
+                layers.append((f"bucket{idx}.p{k}", p.numel(), kind))
+            codecs = resolve_codecs(layers, self.plan, self.filters)
+            segs, off = [], 0
+            for (name, n, _), c in zip(layers, codecs):
+                if c.mode == G.CodecMode.topk:
+                    raise ValueError(f"{name}: the topk codec has no DDP bucket path")
+                segs.append(G.Segment(off, n, c.mode, c.bits, c.bucket_size))
+                off += n
+            red = G.DeviceReducer(self.comm, off, segs)
+            self._reducers[idx] = red
+        return red
+
+    def reduce(self, bucket):
+        buf = bucket.buffer()
+        red = self._reducer(bucket)
+        seed = G.hash_combine(G.hash_combine(self.step_seed, self.step), bucket.index())
+        red.allreduce(buf.data_ptr(), buf.data_ptr(), seed, G.ReduceOp.average,
+                      torch.cuda.current_stream().cuda_stream)
+        self.calls += 1
+        if bucket.is_last():
+            self.step += 1
+        fut = torch.futures.Future()
+        fut.set_result(buf)
+        return fut
+
+
+def cgx_comm_hook(state, bucket):
+    """The function DDP calls per bucket (a named function, returning a
+    torch.futures.Future[torch.Tensor]);
+    ``state`` is the CgxCommHook holding the reducers."""
+    return state.reduce(bucket)
