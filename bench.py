@@ -353,10 +353,13 @@ def run_codec(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_quant32 (K1: fused bucket norms + stochastic quantize + pack, "
                                "one launch per gcx_quantize)", "peak_kind": peak_kind,
-                     "note": "K1 is integer-bound by the reference RNG; with the key prefixes "
-                             "it hashes one SplitMix64 finalizer per element and reads the "
-                             "8-byte prefix T(i) (traffic ~ 4+8 B/elem vs 4.6 algorithmic); "
-                             "config.hash_only_ms is the three-finalizer hash alone",
+                     "note": "K1 is bound by the reference RNG's integer work and its latency, "
+                             "not HBM: with the key prefixes it hashes one SplitMix64 finalizer "
+                             "per element and reads the 8-byte prefix T(i) (traffic ~ 4+8 B/elem "
+                             "vs 4.6 algorithmic); ncu (profiles/round1_c1_k_quant32.md): issue "
+                             "slots 45 % busy, ALU pipe 48 %, long-scoreboard the top stall at "
+                             "25 % occupancy (128 registers); config.hash_only_ms is the "
+                             "three-finalizer hash alone (the inline path's ceiling)",
                      "algorithmic_bytes_per_launch": q_bytes},
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": 4 * n / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
