@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "devmem.hpp"
@@ -304,10 +305,40 @@ struct TableBlob {
 // K1 over a table quantized under one seed: draw the shared key runs once
 // (gcx_make_keys), then norms + quantize + pack reading keys from the table
 // (from the table's stored key prefixes when given: one finalizer per slot)
+// A table whose key slots are NOT shared between pieces (one owner chunk, or
+// N = 2's single peer chunk) and is large is quantized in ONE launch straight
+// from the prefixes (K1 hashes mix64(seed ^ T) per element): the separate
+// key-table pass would hash every slot once anyway and adds its traffic.
+// Shared tables (N > 2 send tables: N-1 pieces read each slot) and small
+// tables (the CTA K1 has the lower latency) keep the two-step path.
+// Measured on B200, 4-bit/128: N = 2 at 16/64 MiB 78 -> 71 / 222 -> 187 us
+// per rank one-step; 4 MiB and below, two-step is 7-9 us faster.
+// GCX_ONESTEP_MIN_SLOTS overrides the size threshold (measurement).
+std::uint64_t onestep_min_slots() {
+  static const std::uint64_t v = [] {
+    const char* e = std::getenv("GCX_ONESTEP_MIN_SLOTS");
+    return e != nullptr ? std::strtoull(e, nullptr, 10) : std::uint64_t{1} << 20;
+  }();
+  return v;
+}
+
+bool onestep(const Table& t) {
+  std::uint64_t q = 0;
+  for (const auto& p : t.pieces)
+    if (p.bits > 0) q += p.len;
+  return t.key_len >= onestep_min_slots() && 2 * q < 3 * t.key_len;
+}
+
 void encode(const TableBlob& blob, const Table& t, std::uint64_t seed, const float* src,
             std::uint8_t* msg, unsigned long long* keys, unsigned long long* bad,
             cudaStream_t st, const unsigned long long* key_prefix = nullptr) {
   const bool use_keys = keys != nullptr && t.key_len > 0;
+  if (use_keys && key_prefix != nullptr && onestep(t)) {
+    gcx_check(gcx_encode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
+                                t.ntiles, t.flags | GCX_F_KEY_PREFIX, seed, src, msg, key_prefix,
+                                bad, st));
+    return;
+  }
   if (use_keys && key_prefix != nullptr)
     gcx_check(gcx_make_keys_prefixed(t.key_len, seed, key_prefix, keys, st));
   else if (use_keys)
