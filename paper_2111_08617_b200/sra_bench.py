@@ -80,7 +80,7 @@ def run(args, metric, ClockSampler, measured_peaks, cpu_codec_sample):
     # end to end with host buffers: pinned H2D of the gradient, reduce, D2H
     host_in = [torch.empty(b.numel(), dtype=torch.float32, pin_memory=True).normal_()
                for b in car.flat]
-    host_out = [torch.empty_like(h) for h in host_in]
+    host_out = [torch.empty(h.numel(), dtype=torch.float32, pin_memory=True) for h in host_in]
     torch.cuda.synchronize()
     dist.barrier()
     x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -112,6 +112,9 @@ def run(args, metric, ClockSampler, measured_peaks, cpu_codec_sample):
                                    "SRA average",
                        "parallelism": f"dp{world}", "buffers": len(car.buffers),
                        "convention": "busbw = (4n/t)*2(N-1)/N (nccl-tests)",
+                       "aggregate_input_GBps": world * 4 * n / (ms * 1e-3) / 1e9,
+                       "aggregate_note": "all ranks' gradient bytes reduced per second "
+                                         "(N x 4n / t)",
                        "nccl_fp32_allreduce_ms": base_ms,
                        "nccl_fp32_busbw_GBps": busbw(base_ms),
                        "speedup_vs_nccl_fp32": base_ms / ms,
