@@ -12,6 +12,6 @@ for name in names:
     shutil.copy(src, lib)
     out = subprocess.run([sys.executable, "bench.py", "--steps", "20", "--warmup", "5"], capture_output=True, text=True, cwd=ROOT).stdout
     d = json.loads(out.strip().splitlines()[-1])
-    res[name] = (d["value"], d["ms_per_step"], d["config"]["ms_per_step_serial"], d["config"]["quantize_ms"])
+    res[name] = (d["value"], d["ms_per_step"], d["config"]["ms_per_step_serial"], d["config"]["quantize_ms"], d["config"]["dequantize_ms"])
     print(name, res[name], flush=True)
 shutil.copy("/tmp/libgcx_orig.so", lib)
