@@ -62,6 +62,10 @@ def _ptrs(arrs):
     return (C.POINTER(C.c_float) * len(arrs))(*[_f32p(a) for a in arrs])
 
 
+def _threads():
+    return max(1, min(32, len(os.sched_getaffinity(0))))
+
+
 def bucket_count(n, bucket):
     return (n + bucket - 1) // bucket
 
@@ -90,6 +94,7 @@ class Oracle:
         L.oc_normal01.restype = flt
         L.oc_normal01.argtypes = [u64, u64]
         L.oc_fill_normal.argtypes = [C.POINTER(flt), u64, u64, flt]
+        L.oc_fill_normal_range.argtypes = [C.POINTER(flt), u64, u64, u64, flt]
         L.oc_fnv1a64.restype = u64
         L.oc_fnv1a64.argtypes = [C.c_void_p, u64]
         L.oc_compressed_size.restype = u64
@@ -132,9 +137,24 @@ class Oracle:
     def normal01(self, s, i):
         return self.lib.oc_normal01(s, i)
 
-    def normal_vector(self, n, seed, scale=1.0):
-        out = np.empty(n, np.float32)
-        self.lib.oc_fill_normal(_f32p(out), n, seed, scale)
+    def normal_vector(self, n, seed, scale=1.0, out=None):
+        if out is None:
+            out = np.empty(n, np.float32)
+        if n < (1 << 20):
+            self.lib.oc_fill_normal(_f32p(out), n, seed, scale)
+            return out
+        # large vectors: ctypes releases the GIL, so threads fill slices
+        from concurrent.futures import ThreadPoolExecutor
+        step = 1 << 20
+        base = out.ctypes.data
+        fp = C.POINTER(C.c_float)
+
+        def fill(lo):
+            m = min(step, n - lo)
+            self.lib.oc_fill_normal_range(C.cast(base + 4 * lo, fp), lo, m, seed, scale)
+
+        with ThreadPoolExecutor(max_workers=_threads()) as ex:
+            list(ex.map(fill, range(0, n, step)))
         return out
 
     def fnv1a64(self, arr):
@@ -361,4 +381,30 @@ def engine_inputs(oracle, layers, nodes, step, tag):
             key = oracle.hash_combine(oracle.hash_combine(oracle.hash_combine(tag, step), r), t)
             row.append(oracle.normal_vector(n, key, scale))
         out.append(row)
+    return out
+
+
+def engine_inputs_flat(oracle, layers, step, tag, rank):
+    """One rank's engine inputs (same recipe as engine_inputs), the layers
+    concatenated into one float32 vector, filled by a thread pool (ctypes
+    releases the GIL) so full-size models take seconds."""
+    from concurrent.futures import ThreadPoolExecutor
+    sizes = [x[1] for x in layers]
+    total = int(sum(sizes))
+    out = np.empty(total, np.float32)
+    base = out.ctypes.data
+    fp = C.POINTER(C.c_float)
+    jobs, off = [], 0
+    for t, (_, n, _, scale) in enumerate(layers):
+        key = oracle.hash_combine(oracle.hash_combine(oracle.hash_combine(tag, step), rank), t)
+        for lo in range(0, n, 1 << 20):
+            jobs.append((off + lo, lo, min(1 << 20, n - lo), key, scale))
+        off += n
+
+    def fill(j):
+        dst, lo, m, key, scale = j
+        oracle.lib.oc_fill_normal_range(C.cast(base + 4 * dst, fp), lo, m, key, scale)
+
+    with ThreadPoolExecutor(max_workers=_threads()) as ex:
+        list(ex.map(fill, jobs))
     return out

@@ -281,37 +281,89 @@ PYBIND11_MODULE(_gcomm, m) {
     out["bytes_sent"] = tr.bytes_sent;
     return out;
   });
+  m.def("sra_exchange_plan", [](std::size_t d, std::size_t nodes, std::size_t me,
+                                std::vector<collectives::Segment> segs) {
+    collectives::validate_segments(segs, d);
+    const auto L = collectives::make_layout(d, nodes, segs);
+    const auto P = collectives::sra_exchange_plan(L, me);
+    static const char* region[] = {"send", "recv", "gather"};
+    py::dict out;
+    out["recv_stride"] = P.recv_stride;
+    out["gather_offset"] = L.gather_offset;
+    out["gather_bytes"] = L.gather_bytes;
+    py::list rounds;
+    for (int r = 0; r < 2; ++r) {
+      py::list sends, recvs;
+      for (const auto& t : P.sends[r])
+        sends.append(py::make_tuple(t.peer, region[int(t.region)], t.offset, t.bytes));
+      for (const auto& t : P.recvs[r])
+        recvs.append(py::make_tuple(t.peer, region[int(t.region)], t.offset, t.bytes));
+      py::dict rd;
+      rd["sends"] = sends;
+      rd["recvs"] = recvs;
+      rounds.append(rd);
+    }
+    out["rounds"] = rounds;
+    return out;
+  }, py::arg("elements"), py::arg("nodes"), py::arg("me"), py::arg("segments"));
   m.def("allreduce", &collectives::allreduce, py::arg("request"), py::arg("nodes"),
         py::call_guard<py::gil_scoped_release>());
   m.def("sparse_allreduce", &collectives::sparse_allreduce, py::arg("chunks"), py::arg("op"),
         py::arg("nodes"), py::call_guard<py::gil_scoped_release>());
 
-  py::class_<collectives::Communicator>(m, "Communicator")
+  py::class_<collectives::Transport>(m, "Transport")
+      .def("rank", &collectives::Transport::rank)
+      .def("size", &collectives::Transport::size)
+      .def("kind", &collectives::Transport::kind)
+      .def("split", &collectives::Transport::split, py::call_guard<py::gil_scoped_release>())
+      .def("check_async", &collectives::Transport::check_async);
+  py::class_<collectives::Communicator, collectives::Transport>(m, "Communicator")
       .def(py::init([](int rank, int nranks, py::bytes id) {
              std::string s = id;
-             return std::make_unique<collectives::Communicator>(
-                 rank, nranks, std::vector<std::uint8_t>(s.begin(), s.end()));
+             std::vector<std::uint8_t> v(s.begin(), s.end());
+             py::gil_scoped_release nogil;
+             return std::make_unique<collectives::Communicator>(rank, nranks, v);
            }),
            py::arg("rank"), py::arg("nranks"), py::arg("unique_id"))
-      .def_static("unique_id",
-                  []() {
-                    const auto id = collectives::Communicator::unique_id();
-                    return py::bytes(reinterpret_cast<const char*>(id.data()), id.size());
-                  })
-      .def("rank", &collectives::Communicator::rank)
-      .def("size", &collectives::Communicator::size);
+      .def_static("unique_id", []() {
+        const auto id = collectives::Communicator::unique_id();
+        return py::bytes(reinterpret_cast<const char*>(id.data()), id.size());
+      });
+  py::class_<collectives::LoopbackHub, std::shared_ptr<collectives::LoopbackHub>>(m, "LoopbackHub")
+      .def(py::init<int, double>(), py::arg("nranks"), py::arg("timeout_s") = 120.0)
+      .def("size", &collectives::LoopbackHub::size)
+      .def("rounds", &collectives::LoopbackHub::rounds)
+      .def("bytes_moved", &collectives::LoopbackHub::bytes_moved)
+      .def("transport", [](std::shared_ptr<collectives::LoopbackHub> hub, int rank) {
+        return std::make_unique<collectives::LoopbackTransport>(hub, rank);
+      }, py::arg("rank"));
+  py::class_<collectives::LoopbackTransport, collectives::Transport>(m, "LoopbackTransport")
+      .def(py::init<std::shared_ptr<collectives::LoopbackHub>, int>(), py::arg("hub"),
+           py::arg("rank"))
+      .def_property_readonly("hub", &collectives::LoopbackTransport::hub);
   py::class_<collectives::DeviceReducer>(m, "DeviceReducer")
-      .def(py::init<collectives::Communicator&, std::size_t, std::vector<collectives::Segment>>(),
-           py::keep_alive<1, 2>())
+      .def(py::init<collectives::Transport&, std::size_t, std::vector<collectives::Segment>>(),
+           py::arg("transport"), py::arg("elements"), py::arg("segments"), py::keep_alive<1, 2>())
       .def(
           "allreduce",
           [](collectives::DeviceReducer& r, std::uintptr_t in, std::uintptr_t out,
-             std::uint64_t step_seed, collectives::ReduceOp op, std::uintptr_t stream) {
+             std::uint64_t elements, std::uint64_t step_seed, collectives::ReduceOp op,
+             std::uintptr_t stream) {
+            // the reducer's layout is fixed: a buffer of another length would
+            // be read and written out of bounds (advisor finding, ddp hook)
+            if (elements != r.elements())
+              throw std::invalid_argument("buffer holds " + std::to_string(elements) +
+                                          " elements but the reducer was built for " +
+                                          std::to_string(r.elements()));
+            py::gil_scoped_release nogil;  // loopback ranks rendezvous across threads
             r.allreduce(reinterpret_cast<const float*>(in), reinterpret_cast<float*>(out),
                         step_seed, op, reinterpret_cast<void*>(stream));
           },
-          py::arg("in_ptr"), py::arg("out_ptr"), py::arg("step_seed"), py::arg("op"),
-          py::arg("stream") = 0)
+          py::arg("in_ptr"), py::arg("out_ptr"), py::arg("elements"), py::arg("step_seed"),
+          py::arg("op"), py::arg("stream") = 0)
+      .def("poll", &collectives::DeviceReducer::poll, py::arg("wait") = true,
+           py::call_guard<py::gil_scoped_release>())
+      .def("elements", &collectives::DeviceReducer::elements)
       .def("trace", &collectives::DeviceReducer::trace)
       .def("device_bytes_sent", &collectives::DeviceReducer::device_bytes_sent)
       .def("launches_per_call", &collectives::DeviceReducer::launches_per_call)

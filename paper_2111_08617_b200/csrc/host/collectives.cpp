@@ -9,8 +9,12 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <thread>
 
 #include "devmem.hpp"
 #include "gcomm.hpp"
@@ -102,14 +106,9 @@ void StepTrace::accumulate(const StepTrace& o) {
 }
 
 // collectives.cpp:77-102 (same messages)
-void validate_request(const ReduceRequest& req, std::size_t nodes) {
-  if (req.inputs.size() != nodes)
-    throw std::invalid_argument("expected one input buffer per node");
-  const std::size_t d = req.inputs.empty() ? 0 : req.inputs[0].size();
-  for (const auto& in : req.inputs)
-    if (in.size() != d) throw std::invalid_argument("input buffers must have equal lengths");
+void validate_segments(const std::vector<Segment>& segments, std::size_t d) {
   std::size_t cursor = 0;
-  for (const auto& seg : req.segments) {
+  for (const auto& seg : segments) {
     if (seg.offset != cursor)
       throw std::invalid_argument("segments must cover the buffer contiguously");
     if (seg.length == 0) throw std::invalid_argument("zero-length segment");
@@ -128,6 +127,15 @@ void validate_request(const ReduceRequest& req, std::size_t nodes) {
   if (cursor != d)
     throw std::invalid_argument("segments cover " + std::to_string(cursor) +
                                 " elements but buffers hold " + std::to_string(d));
+}
+
+void validate_request(const ReduceRequest& req, std::size_t nodes) {
+  if (req.inputs.size() != nodes)
+    throw std::invalid_argument("expected one input buffer per node");
+  const std::size_t d = req.inputs.empty() ? 0 : req.inputs[0].size();
+  for (const auto& in : req.inputs)
+    if (in.size() != d) throw std::invalid_argument("input buffers must have equal lengths");
+  validate_segments(req.segments, d);
 }
 
 // collectives.cpp:106-122
@@ -815,7 +823,7 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
 }
 
 // ---------------------------------------------------------------------------
-// one rank per GPU over NCCL
+// transports
 // ---------------------------------------------------------------------------
 std::vector<std::uint8_t> Communicator::unique_id() {
   ncclUniqueId id;
@@ -839,6 +847,186 @@ Communicator::~Communicator() {
   if (comm_) ncclCommDestroy(static_cast<ncclComm_t>(comm_));
 }
 
+void Communicator::exchange(const std::vector<PeerTransfer>& sends,
+                            const std::vector<PeerTransfer>& recvs, void* stream) {
+  ncclComm_t comm = static_cast<ncclComm_t>(comm_);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  nccl_check(ncclGroupStart(), "ncclGroupStart");
+  for (const auto& t : sends)
+    nccl_check(ncclSend(t.src, t.bytes, ncclUint8, t.peer, comm, st), "ncclSend");
+  for (const auto& t : recvs)
+    nccl_check(ncclRecv(t.dst, t.bytes, ncclUint8, t.peer, comm, st), "ncclRecv");
+  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+}
+
+std::unique_ptr<Transport> Communicator::split() {
+  ncclComm_t child = nullptr;
+  nccl_check(ncclCommSplit(static_cast<ncclComm_t>(comm_), 0, rank_, &child, nullptr),
+             "ncclCommSplit");
+  return std::unique_ptr<Transport>(new Communicator(rank_, nranks_, child));
+}
+
+void Communicator::check_async() {
+  ncclResult_t r = ncclSuccess;
+  nccl_check(ncclCommGetAsyncError(static_cast<ncclComm_t>(comm_), &r), "ncclCommGetAsyncError");
+  if (r != ncclSuccess && r != ncclInProgress)
+    throw std::runtime_error(std::string("NCCL asynchronous error: ") + ncclGetErrorString(r));
+}
+
+struct LoopbackHub::Impl {
+  struct Posted {
+    std::vector<PeerTransfer> sends, recvs;
+  };
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  std::uint64_t gen = 0;
+  std::vector<Posted> posted;
+  std::vector<cudaEvent_t> ready, done;
+  std::vector<std::shared_ptr<LoopbackHub>> children;
+  std::vector<std::size_t> nsplit;
+};
+
+LoopbackHub::LoopbackHub(int nranks, double timeout_s)
+    : n_(nranks), timeout_s_(timeout_s), impl_(std::make_unique<Impl>()) {
+  if (nranks < 1) throw std::invalid_argument("loopback needs at least one rank");
+  impl_->posted.resize(nranks);
+  impl_->ready.assign(nranks, nullptr);
+  impl_->done.assign(nranks, nullptr);
+  impl_->nsplit.assign(nranks, 0);
+}
+
+LoopbackHub::~LoopbackHub() {
+  for (auto e : impl_->ready)
+    if (e) cudaEventDestroy(e);
+  for (auto e : impl_->done)
+    if (e) cudaEventDestroy(e);
+}
+
+void LoopbackHub::barrier() {
+  Impl& I = *impl_;
+  std::unique_lock<std::mutex> lk(I.mu);
+  const std::uint64_t g = I.gen;
+  if (++I.arrived == n_) {
+    I.arrived = 0;
+    ++I.gen;
+    I.cv.notify_all();
+    return;
+  }
+  if (!I.cv.wait_for(lk, std::chrono::duration<double>(timeout_s_), [&] { return I.gen != g; }))
+    throw std::runtime_error("loopback transport: peers did not reach the exchange within " +
+                             std::to_string(timeout_s_) + " s");
+}
+
+std::shared_ptr<LoopbackHub> LoopbackHub::child(int rank) {
+  Impl& I = *impl_;
+  std::lock_guard<std::mutex> lk(I.mu);
+  const std::size_t k = I.nsplit.at(std::size_t(rank))++;
+  while (I.children.size() <= k) I.children.push_back(std::make_shared<LoopbackHub>(n_, timeout_s_));
+  return I.children[k];
+}
+
+// One round for `rank` (its own host thread).  Sends are matched to
+// receives exactly as NCCL matches grouped ncclSend/ncclRecv (one message per
+// ordered pair, equal sizes); every rank checks the whole round, so a
+// mismatch raises the same error on all of them.  The receiver copies from
+// the sender's buffer after the sender's stream reached the round (event
+// `ready`), and the sender's stream continues only after every receiver
+// copied (event `done`): the send buffer is reusable and the receive buffer
+// full when the stream leaves the round.
+void LoopbackHub::exchange(int rank, const std::vector<PeerTransfer>& sends,
+                           const std::vector<PeerTransfer>& recvs, void* stream) {
+  Impl& I = *impl_;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const std::size_t me = std::size_t(rank);
+  if (!I.ready[me]) {
+    cuda_check(cudaEventCreateWithFlags(&I.ready[me], cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&I.done[me], cudaEventDisableTiming), "event");
+  }
+  I.posted[me].sends = sends;
+  I.posted[me].recvs = recvs;
+  cuda_check(cudaEventRecord(I.ready[me], st), "event record");
+  barrier();
+  auto find = [](const std::vector<PeerTransfer>& v, int peer) -> const PeerTransfer* {
+    const PeerTransfer* hit = nullptr;
+    for (const auto& t : v)
+      if (t.peer == peer) {
+        if (hit) throw std::runtime_error("loopback transport: two messages for one peer in a round");
+        hit = &t;
+      }
+    return hit;
+  };
+  for (int r = 0; r < n_; ++r)
+    for (const auto& rv : I.posted[std::size_t(r)].recvs) {
+      if (rv.peer < 0 || rv.peer >= n_ || rv.peer == r)
+        throw std::runtime_error("loopback transport: bad peer " + std::to_string(rv.peer));
+      const PeerTransfer* sd = find(I.posted[std::size_t(rv.peer)].sends, r);
+      if (!sd || sd->bytes != rv.bytes)
+        throw std::runtime_error("loopback transport: rank " + std::to_string(r) + " expects " +
+                                 std::to_string(rv.bytes) + " bytes from rank " +
+                                 std::to_string(rv.peer) + ", which sends " +
+                                 (sd ? std::to_string(sd->bytes) : std::string("nothing")));
+    }
+  for (int r = 0; r < n_; ++r)
+    for (const auto& sd : I.posted[std::size_t(r)].sends)
+      if (sd.peer < 0 || sd.peer >= n_ || !find(I.posted[std::size_t(sd.peer)].recvs, r))
+        throw std::runtime_error("loopback transport: rank " + std::to_string(r) +
+                                 " sends to rank " + std::to_string(sd.peer) +
+                                 ", which posted no receive");
+  std::uint64_t moved = 0;
+  for (const auto& rv : recvs) {
+    const PeerTransfer* sd = find(I.posted[std::size_t(rv.peer)].sends, rank);
+    cuda_check(cudaStreamWaitEvent(st, I.ready[std::size_t(rv.peer)], 0), "stream wait");
+    if (rv.bytes)
+      cuda_check(cudaMemcpyAsync(rv.dst, sd->src, rv.bytes, cudaMemcpyDeviceToDevice, st),
+                 "loopback copy");
+    moved += rv.bytes;
+  }
+  cuda_check(cudaEventRecord(I.done[me], st), "event record");
+  barrier();
+  for (const auto& sd : sends)
+    cuda_check(cudaStreamWaitEvent(st, I.done[std::size_t(sd.peer)], 0), "stream wait");
+  std::lock_guard<std::mutex> lk(I.mu);
+  bytes_ += moved;
+  if (rank == 0) ++rounds_;
+}
+
+LoopbackTransport::LoopbackTransport(std::shared_ptr<LoopbackHub> hub, int rank)
+    : hub_(std::move(hub)), rank_(rank) {
+  if (!hub_) throw std::invalid_argument("loopback transport needs a hub");
+  if (rank < 0 || rank >= hub_->size())
+    throw std::invalid_argument("loopback rank " + std::to_string(rank) + " outside [0, " +
+                                std::to_string(hub_->size()) + ")");
+}
+
+std::unique_ptr<Transport> LoopbackTransport::split() {
+  return std::make_unique<LoopbackTransport>(hub_->child(rank_), rank_);
+}
+
+ExchangePlan sra_exchange_plan(const SraLayout& L, std::size_t me) {
+  const std::size_t N = L.nodes;
+  ExchangePlan P;
+  if (N <= 1) return P;
+  const std::uint64_t m_me = L.chunks[me].msg_bytes;
+  P.recv_stride = align_up(std::max<std::uint64_t>(m_me, 16), kMsgAlign);
+  for (std::size_t j = 1; j < N; ++j) {
+    const std::size_t peer = (me + j) % N, src = (me + N - j) % N;
+    // round 1: my share of owner `peer`'s chunk; owner me receives src's share
+    if (L.chunks[peer].msg_bytes)
+      P.sends[0].push_back({int(peer), Region::send, L.gather_offset[peer], L.chunks[peer].msg_bytes});
+    if (m_me)
+      P.recvs[0].push_back({int(src), Region::recv, (src < me ? src : src - 1) * P.recv_stride, m_me});
+    // round 2: my compressed aggregate to everybody; src's aggregate to me
+    if (m_me) P.sends[1].push_back({int(peer), Region::gather, L.gather_offset[me], m_me});
+    if (L.chunks[src].msg_bytes)
+      P.recvs[1].push_back({int(src), Region::gather, L.gather_offset[src], L.chunks[src].msg_bytes});
+  }
+  return P;
+}
+
+// ---------------------------------------------------------------------------
+// one rank per GPU
+// ---------------------------------------------------------------------------
 struct DeviceReducer::Impl {
   Table send, own, dec;
   TableBlob blob;
@@ -846,35 +1034,25 @@ struct DeviceReducer::Impl {
   DeviceBuffer prefix_send, prefix_own;  // seed-independent key prefixes, built once
   std::uint64_t recv_stride = 0;
   std::uint32_t flags = 0;
+  ExchangePlan plan;
+  std::vector<PeerTransfer> sends[2], recvs[2];  // the plan as device pointers
+  // non-finite flags of the last call, copied to pinned host memory at its end
+  unsigned long long* host_bad = nullptr;
+  cudaEvent_t done = nullptr;
+  bool pending = false;
+  ~Impl() {
+    if (host_bad) cudaFreeHost(host_bad);
+    if (done) cudaEventDestroy(done);
+  }
 };
 
-DeviceReducer::DeviceReducer(Communicator& comm, std::size_t d, std::vector<Segment> segments)
-    : comm_(comm), impl_(std::make_unique<Impl>()) {
-  ReduceRequest probe;
-  probe.segments = segments;
-  probe.inputs.assign(1, {});
-  // validate the segment table without materialising inputs
-  std::size_t cursor = 0;
-  for (const auto& seg : segments) {
-    if (seg.offset != cursor)
-      throw std::invalid_argument("segments must cover the buffer contiguously");
-    if (seg.length == 0) throw std::invalid_argument("zero-length segment");
-    if (seg.mode == model::CodecMode::topk)
-      throw std::invalid_argument("topk segments use the sparse path");
-    if (seg.mode == model::CodecMode::quantize) {
-      codec::QuantParams p;
-      p.bits = seg.bits;
-      p.bucket_size = seg.bucket_size;
-      p.validate();
-    }
-    cursor += seg.length;
-  }
-  if (cursor != d)
-    throw std::invalid_argument("segments cover " + std::to_string(cursor) +
-                                " elements but buffers hold " + std::to_string(d));
-  const std::size_t N = std::size_t(comm.size()), me = std::size_t(comm.rank());
+DeviceReducer::DeviceReducer(Transport& transport, std::size_t d, std::vector<Segment> segments)
+    : transport_(transport), impl_(std::make_unique<Impl>()) {
+  validate_segments(segments, d);
+  const std::size_t N = std::size_t(transport.size()), me = std::size_t(transport.rank());
   layout_ = make_layout(d, N, segments);
   if (N == 1) return;
+  detail::require_device();
   Impl& I = *impl_;
   for (std::size_t c = 0; c < N; ++c) {
     if (c != me) append(I.send, layout_.chunks[c].pieces, layout_.gather_offset[c]);
@@ -894,12 +1072,25 @@ DeviceReducer::DeviceReducer(Communicator& comm, std::size_t d, std::vector<Segm
   gcx_check(gcx_make_key_prefix(I.blob.groups(I.own), std::uint32_t(I.own.groups.size()),
                                 I.own.key_len, I.prefix_own.get<unsigned long long>(), nullptr));
   cuda_check(cudaDeviceSynchronize(), "key prefixes");
-  I.recv_stride = align_up(std::max<std::uint64_t>(layout_.chunks[me].msg_bytes, 16), kMsgAlign);
+  I.plan = sra_exchange_plan(layout_, me);
+  I.recv_stride = I.plan.recv_stride;
   I.send_buf.reset(layout_.gather_bytes + 16);
   I.gather_buf.reset(layout_.gather_bytes + 16);
   I.recv_buf.reset(I.recv_stride * (N - 1) + 16);
   I.bad.reset(16);
   cuda_check(cudaMemset(I.bad.get(), 0xFF, 16), "memset");
+  cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&I.host_bad), 16, cudaHostAllocDefault),
+             "cudaHostAlloc");
+  I.host_bad[0] = I.host_bad[1] = ~0ULL;
+  cuda_check(cudaEventCreateWithFlags(&I.done, cudaEventDisableTiming), "event");
+  std::uint8_t* base[3] = {I.send_buf.get<std::uint8_t>(), I.recv_buf.get<std::uint8_t>(),
+                           I.gather_buf.get<std::uint8_t>()};
+  for (int r = 0; r < 2; ++r) {
+    for (const auto& t : I.plan.sends[r])
+      I.sends[r].push_back({t.peer, base[int(t.region)] + t.offset, nullptr, t.bytes});
+    for (const auto& t : I.plan.recvs[r])
+      I.recvs[r].push_back({t.peer, nullptr, base[int(t.region)] + t.offset, t.bytes});
+  }
   if (I.flags & GCX_F_NEEDS_ZERO) {
     cuda_check(cudaMemset(I.send_buf.get(), 0, I.send_buf.size()), "memset");
     cuda_check(cudaMemset(I.gather_buf.get(), 0, I.gather_buf.size()), "memset");
@@ -911,15 +1102,15 @@ DeviceReducer::~DeviceReducer() = default;
 void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_seed, ReduceOp op,
                               void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const std::size_t N = layout_.nodes, me = std::size_t(comm_.rank()), d = layout_.d;
-  if (N == 1) {
+  const std::size_t N = layout_.nodes, me = std::size_t(transport_.rank()), d = layout_.d;
+  if (N == 1) {  // collectives.cpp:479-486: identity, nothing compressed
     if (in != out)
       cuda_check(cudaMemcpyAsync(out, in, 4 * d, cudaMemcpyDeviceToDevice, st), "copy");
     return;
   }
   Impl& I = *impl_;
-  ncclComm_t comm = static_cast<ncclComm_t>(comm_.handle());
   const float divisor = op == ReduceOp::average ? float(N) : 1.0f;
+  cuda_check(cudaMemsetAsync(I.bad.get(), 0xFF, 16, st), "memset");
   if (I.flags & GCX_F_NEEDS_ZERO) {
     cuda_check(cudaMemsetAsync(I.send_buf.get(), 0, I.send_buf.size(), st), "memset");
     cuda_check(cudaMemsetAsync(I.gather_buf.get<std::uint8_t>() + layout_.gather_offset[me], 0,
@@ -928,25 +1119,13 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
   auto* bad = I.bad.get<unsigned long long>();
   auto* keys = I.keys.get<unsigned long long>();
   // K1: my share of every other owner's chunk, seed hop_seed(step, 0, me)
+  // (collectives.cpp:252-253)
   encode(I.blob, I.send, hop_seed(step_seed, 0, me), in, I.send_buf.get<std::uint8_t>(), keys,
          bad, st, I.prefix_send.get<unsigned long long>());
-  // round 1: all-to-all of compressed chunks
-  const std::uint64_t m_me = layout_.chunks[me].msg_bytes;
-  nccl_check(ncclGroupStart(), "ncclGroupStart");
-  for (std::size_t j = 1; j < N; ++j) {
-    const std::size_t peer = (me + j) % N;
-    const std::size_t src = (me + N - j) % N;
-    if (layout_.chunks[peer].msg_bytes)
-      nccl_check(ncclSend(I.send_buf.get<std::uint8_t>() + layout_.gather_offset[peer],
-                          layout_.chunks[peer].msg_bytes, ncclUint8, int(peer), comm, st),
-                 "ncclSend");
-    if (m_me)
-      nccl_check(ncclRecv(I.recv_buf.get<std::uint8_t>() + (src < me ? src : src - 1) * I.recv_stride,
-                          m_me, ncclUint8, int(src), comm, st),
-                 "ncclRecv");
-  }
-  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  // round 1: all-to-all of compressed chunks (collectives.cpp:255, :264)
+  transport_.exchange(I.sends[0], I.recvs[0], st);
   // K2: ascending-id fold into out, then re-encode with the hop-1 seed
+  // (collectives.cpp:266-284)
   std::uint8_t* bcast = I.gather_buf.get<std::uint8_t>() + layout_.gather_offset[me];
   gcx_check(gcx_fold_pieces(I.blob.pieces(I.own), I.blob.prefix(I.own),
                             std::uint32_t(I.own.pieces.size()), I.own.ntiles, I.own.flags,
@@ -955,36 +1134,42 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
   encode(I.blob, I.own, hop_seed(step_seed, 1, me), out, bcast, keys, bad + 1, st,
          I.prefix_own.get<unsigned long long>());
   // round 2: variable-size all-gather of the owners' compressed aggregates
-  nccl_check(ncclGroupStart(), "ncclGroupStart");
-  for (std::size_t j = 1; j < N; ++j) {
-    const std::size_t peer = (me + j) % N;
-    const std::size_t src = (me + N - j) % N;
-    if (m_me) nccl_check(ncclSend(bcast, m_me, ncclUint8, int(peer), comm, st), "ncclSend");
-    if (layout_.chunks[src].msg_bytes)
-      nccl_check(ncclRecv(I.gather_buf.get<std::uint8_t>() + layout_.gather_offset[src],
-                          layout_.chunks[src].msg_bytes, ncclUint8, int(src), comm, st),
-                 "ncclRecv");
-  }
-  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  // (collectives.cpp:289, :297)
+  transport_.exchange(I.sends[1], I.recvs[1], st);
   // K3: decode every owner's chunk (own included) (+ average)
   gcx_check(gcx_decode_pieces(I.blob.pieces(I.dec), I.blob.prefix(I.dec),
                               std::uint32_t(I.dec.pieces.size()), I.dec.ntiles, I.dec.flags,
                               I.gather_buf.get<std::uint8_t>(), out, divisor, st));
+  cuda_check(cudaMemcpyAsync(I.host_bad, I.bad.get(), 16, cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaEventRecord(I.done, st), "event record");
+  I.pending = true;
 }
 
-StepTrace DeviceReducer::trace() const {
-  StepTrace t = sra_trace(layout_);
-  if (impl_ && layout_.nodes > 1) {
-    std::uint64_t bad[2];
-    cuda_check(cudaMemcpy(bad, impl_->bad.get(), 16, cudaMemcpyDeviceToHost), "D2H");
-    for (int k = 0; k < 2; ++k)
-      if (bad[k] != ~0ULL) throw_non_finite(k == 0 ? impl_->send : impl_->own, bad[k]);
+bool DeviceReducer::poll(bool wait) {
+  if (layout_.nodes <= 1 || !impl_->pending) return true;
+  Impl& I = *impl_;
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(I.done);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) cuda_check(q, "cudaEventQuery");
+    transport_.check_async();
+    if (!wait) return false;
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
   }
-  return t;
+  I.pending = false;
+  for (int k = 0; k < 2; ++k)
+    if (I.host_bad[k] != ~0ULL) {
+      const unsigned long long key = I.host_bad[k];
+      I.host_bad[0] = I.host_bad[1] = ~0ULL;
+      throw_non_finite(k == 0 ? I.send : I.own, key);
+    }
+  return true;
 }
+
+StepTrace DeviceReducer::trace() const { return sra_trace(layout_); }
 
 std::uint64_t DeviceReducer::device_bytes_sent() const {
-  const std::size_t N = layout_.nodes, me = std::size_t(comm_.rank());
+  const std::size_t N = layout_.nodes, me = std::size_t(transport_.rank());
   std::uint64_t b = 0;
   for (std::size_t c = 0; c < N; ++c)
     if (c != me) b += layout_.chunks[c].msg_bytes + layout_.chunks[me].msg_bytes;

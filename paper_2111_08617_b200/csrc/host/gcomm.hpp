@@ -223,41 +223,164 @@ ReduceResult allreduce(const ReduceRequest& request, std::size_t nodes);
 ReduceResult sparse_allreduce(const std::vector<codec::SparseChunk>& chunks, ReduceOp op,
                               std::size_t nodes);
 
-// ---------------- one process per GPU (NCCL over NVLink) ----------------
-class Communicator {
+// ---------------- one process per GPU ----------------
+// One rank's view of the exchange fabric.  DeviceReducer drives its two SRA
+// rounds (collectives.cpp:255,264 / :289,297 in the reference) through this
+// interface, so every offset, slot and message size is computed once and the
+// fabric only moves bytes:
+//   Communicator       NCCL grouped ncclSend/ncclRecv over NVLink (production)
+//   LoopbackTransport  N in-process ranks on ONE GPU, one host thread each;
+//                      a round is a device-to-device copy from the sender's
+//                      buffer into the receiver's (same descriptors, same
+//                      matching rule as NCCL), so the production per-rank
+//                      path runs at N > 1 on a single B200.
+struct PeerTransfer {
+  int peer = 0;
+  const void* src = nullptr;  // sends: the bytes to send
+  void* dst = nullptr;        // receives: where they land
+  std::uint64_t bytes = 0;
+};
+
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  virtual int rank() const = 0;
+  virtual int size() const = 0;
+  virtual std::string kind() const = 0;
+  // One round, issued on `stream` (a cudaStream_t) with NCCL grouped
+  // semantics: when the stream reaches the end of the round every receive
+  // buffer holds its message and every send buffer may be reused.  Each
+  // (sender, receiver) pair carries at most one message per round; sizes
+  // must agree on both sides (std::runtime_error otherwise).
+  virtual void exchange(const std::vector<PeerTransfer>& sends,
+                        const std::vector<PeerTransfer>& recvs, void* stream) = 0;
+  // A transport over the same ranks whose rounds are independent of this
+  // one's (a separate stream of messages), for per-buffer pipelining.
+  // Collective: every rank calls it, in the same order.
+  virtual std::unique_ptr<Transport> split() = 0;
+  // Raise asynchronous fabric errors (ncclCommGetAsyncError).
+  virtual void check_async() {}
+};
+
+class Communicator : public Transport {
  public:
   static std::vector<std::uint8_t> unique_id();  // ncclGetUniqueId (128 bytes)
   Communicator(int rank, int nranks, const std::vector<std::uint8_t>& id);
-  ~Communicator();
+  ~Communicator() override;
   Communicator(const Communicator&) = delete;
   Communicator& operator=(const Communicator&) = delete;
-  int rank() const { return rank_; }
-  int size() const { return nranks_; }
+  int rank() const override { return rank_; }
+  int size() const override { return nranks_; }
+  std::string kind() const override { return "nccl"; }
+  void exchange(const std::vector<PeerTransfer>& sends, const std::vector<PeerTransfer>& recvs,
+                void* stream) override;
+  std::unique_ptr<Transport> split() override;  // ncclCommSplit(color 0, key rank)
+  void check_async() override;
   void* handle() const { return comm_; }
 
  private:
+  Communicator(int rank, int nranks, void* comm) : rank_(rank), nranks_(nranks), comm_(comm) {}
   int rank_ = 0, nranks_ = 1;
   void* comm_ = nullptr;
 };
 
-// Per-rank SRA over NCCL for one fixed buffer layout: K1 encode -> grouped
-// send/recv (all-to-all) -> K2 fold+requant -> grouped send/recv
-// (all-gather) -> K3 decode.  Buffers and device piece tables are built once.
+// Shared state of N loopback ranks (one per host thread, one device).
+class LoopbackHub {
+ public:
+  explicit LoopbackHub(int nranks, double timeout_s = 120.0);
+  ~LoopbackHub();
+  LoopbackHub(const LoopbackHub&) = delete;
+  LoopbackHub& operator=(const LoopbackHub&) = delete;
+  int size() const { return n_; }
+  void exchange(int rank, const std::vector<PeerTransfer>& sends,
+                const std::vector<PeerTransfer>& recvs, void* stream);
+  std::shared_ptr<LoopbackHub> child(int rank);  // the rank's next split
+  std::uint64_t rounds() const { return rounds_; }
+  std::uint64_t bytes_moved() const { return bytes_; }
+
+ private:
+  void barrier();
+  struct Impl;
+  int n_;
+  double timeout_s_;
+  std::unique_ptr<Impl> impl_;
+  std::uint64_t rounds_ = 0, bytes_ = 0;
+};
+
+class LoopbackTransport : public Transport {
+ public:
+  LoopbackTransport(std::shared_ptr<LoopbackHub> hub, int rank);
+  int rank() const override { return rank_; }
+  int size() const override { return hub_->size(); }
+  std::string kind() const override { return "loopback"; }
+  void exchange(const std::vector<PeerTransfer>& sends, const std::vector<PeerTransfer>& recvs,
+                void* stream) override {
+    hub_->exchange(rank_, sends, recvs, stream);
+  }
+  std::unique_ptr<Transport> split() override;
+  const std::shared_ptr<LoopbackHub>& hub() const { return hub_; }
+
+ private:
+  std::shared_ptr<LoopbackHub> hub_;
+  int rank_;
+};
+
+// The byte-level plan of one rank's two SRA rounds, from the layout alone
+// (every rank derives it without talking to the others; the reference's
+// node program sends/receives at collectives.cpp:255,264 and :289,297).
+// Offsets are into the rank's three device buffers: `send` (its compressed
+// share of every other chunk, at gather offsets), `recv` (N-1 slots of
+// recv_stride bytes: the chunk from node src lands in slot
+// src < me ? src : src-1) and `gather` (every owner's aggregate at its
+// gather offset; the rank's own is the round-2 send).
+enum class Region { send = 0, recv = 1, gather = 2 };
+struct PlannedTransfer {
+  int peer = 0;
+  Region region = Region::send;
+  std::uint64_t offset = 0;
+  std::uint64_t bytes = 0;
+};
+struct ExchangePlan {
+  std::uint64_t recv_stride = 0;
+  std::vector<PlannedTransfer> sends[2], recvs[2];  // [round]
+};
+ExchangePlan sra_exchange_plan(const SraLayout& layout, std::size_t me);
+
+// Segment-table checks shared by validate_request and DeviceReducer
+// (collectives.cpp:77-102): contiguous cover of [0, d), no empty or topk
+// segments, valid QuantParams, bucket sizes that fit the 32-bit piece field.
+void validate_segments(const std::vector<Segment>& segments, std::size_t d);
+
+// Per-rank SRA for one fixed buffer layout: K1 encode -> round 1 (all-to-all
+// of compressed chunks) -> K2 fold + hop-1 re-encode -> round 2 (variable-size
+// all-gather) -> K3 decode (+ average).  Buffers, device piece tables and key
+// prefixes are built once.  Not reentrant (like the reference's SimNet and an
+// NCCL communicator); concurrent buffers use separate reducers on split
+// transports.
 class DeviceReducer {
  public:
-  DeviceReducer(Communicator& comm, std::size_t d, std::vector<Segment> segments);
+  DeviceReducer(Transport& transport, std::size_t d, std::vector<Segment> segments);
   ~DeviceReducer();
-  // in/out: device pointers to d floats (may alias); stream: cudaStream_t
+  // in/out: device pointers to d floats (may alias); stream: cudaStream_t.
+  // Non-finite inputs of quantized pieces are recorded on the device (the
+  // reference's codec.cpp:43-45 check) and raised by poll().
   void allreduce(const float* in, float* out, std::uint64_t step_seed, ReduceOp op,
                  void* stream);
+  // Raise std::invalid_argument("non-finite gradient value at index i") if
+  // the last completed call saw one, and the transport's async errors.
+  // wait = false: only if that call has finished on the device (no sync).
+  // Returns whether the last call has completed.
+  bool poll(bool wait);
+  std::size_t elements() const { return layout_.d; }
   const SraLayout& layout() const { return layout_; }
   StepTrace trace() const;
   std::uint64_t device_bytes_sent() const;
   int launches_per_call() const;
+  Transport& transport() const { return transport_; }
 
  private:
   struct Impl;
-  Communicator& comm_;
+  Transport& transport_;
   SraLayout layout_;
   std::unique_ptr<Impl> impl_;
 };

@@ -2,8 +2,8 @@
 per-rank fused-buffer engine in ddp.py) at world size 1 on the single GPU the
 test tier has: it must build its NCCL communicator, piece tables and buffers
 for the ResNet-50 layout and behave as the reference's N = 1 allreduce, the
-identity (collectives.cpp:479-486).  The N > 1 exchange is proven bit-exact
-by test_gpu_sra.py, which drives the same layout and kernels on one GPU."""
+identity (collectives.cpp:479-486).  The N > 1 per-rank path is proven
+bit-exact by test_gpu_loopback.py (the same reducers over LoopbackTransport)."""
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -34,7 +34,7 @@ def test_world1_reducer_is_identity():
     red = G.DeviceReducer(comm, 1000, [G.Segment(0, 1000, G.CodecMode.quantize, 4, 128)])
     x = torch.randn(1000, device="cuda")
     y = torch.empty_like(x)
-    red.allreduce(x.data_ptr(), y.data_ptr(), 7, G.ReduceOp.average,
+    red.allreduce(x.data_ptr(), y.data_ptr(), 1000, 7, G.ReduceOp.average,
                   torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert torch.equal(x, y)

@@ -9,7 +9,8 @@ import os
 import numpy as np
 import pytest
 
-from oracle import RefOracle, engine_inputs
+from oracle import RefOracle, engine_inputs, engine_inputs_flat
+from tests.model_cases import cases as model_cases, layers as model_layers
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -28,7 +29,7 @@ KINDS = ["weight", "bias", "norm", "embedding", "other"]
 
 
 def run_engine(g, oracle, nodes, layers, steps, tag, plan_json=None, adaptive_json=None,
-               step_seed=1, fuse_limit=0):
+               step_seed=1, fuse_limit=0, flat_inputs=False):
     cfg = g.EngineConfig()
     cfg.nodes = nodes
     cfg.step_seed = step_seed
@@ -41,8 +42,15 @@ def run_engine(g, oracle, nodes, layers, steps, tag, plan_json=None, adaptive_js
         cfg.adaptive = g.AdaptiveConfig.from_json(adaptive_json)
     eng = g.Engine(cfg)
     digests = []
+    offs = np.cumsum([0] + [x[1] for x in layers])
     for k in range(steps):
-        ins = engine_inputs(oracle, layers, nodes, k, tag)
+        if flat_inputs:  # full-size models: one threaded fill per rank
+            ins = []
+            for r in range(nodes):
+                flat = engine_inputs_flat(oracle, layers, k, tag, r)
+                ins.append([flat[offs[t]:offs[t + 1]] for t in range(len(layers))])
+        else:
+            ins = engine_inputs(oracle, layers, nodes, k, tag)
         for r in range(nodes):
             for t, (name, n, kind, _) in enumerate(layers):
                 eng.submit(r, g.GradientTensor(g.LayerSpec(name, n, getattr(g.LayerKind, KINDS[kind])),
@@ -217,3 +225,29 @@ def test_engine_topk_layers_match_reference(g, oracle, nodes):
     got, _ = run_engine(g, oracle, nodes, layers, 4, 0x7A, plan)
     want, _ = RefOracle().engine_run(nodes, layers, 4, 0x7A, plan)
     assert got == want
+
+
+def _models_golden(name):
+    with open(os.path.join(GOLD, "models.json")) as f:
+        for c in json.load(f)["cases"]:
+            if c["name"] == name:
+                return c
+    pytest.fail(f"{name} missing from tests/golden/models.json")
+
+
+@pytest.mark.parametrize("case", [c for c in model_cases() if c["model"] == "bert_base"],
+                         ids=lambda c: c["name"])
+def test_engine_bert_base_adaptive_matches_reference(g, oracle, case):
+    """C4: BERT-base (206 tensors, 110 M elements) through the Engine with the
+    adaptive k-means planner (palette {2,3,4,5,6,8}, alpha 1) at N = 8: the
+    observation window's statistics (K4), the plan built from them (bit
+    widths per layer, logged as plan_swap) and every step's averaged
+    gradients equal the compiled reference Engine's
+    (src/engine.cpp:147-311, src/adaptive.cpp:417-474)."""
+    want = _models_golden(case["name"])
+    got, eng = run_engine(g, oracle, case["nodes"], model_layers(case["model"]), case["steps"],
+                          case["tag"], None, case["adaptive"], flat_inputs=True)
+    swaps = [json.loads(line) for line in eng.events_json().splitlines()
+             if json.loads(line)["event"] == "plan_swap"]
+    assert [[s["step"], s["payload"]["bits"]] for s in swaps] == want["plan_swaps"]
+    assert got == want["digests"]

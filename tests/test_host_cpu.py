@@ -202,3 +202,44 @@ def test_compute_entry_points_fail_loudly_without_gpu(g):
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         g.quantize(np.ones(10, np.float32), g.QuantParams())
+
+
+@pytest.mark.parametrize("nodes", [2, 3, 4, 5, 8])
+def test_exchange_plans_pair_up_across_ranks(g, nodes):
+    """sra_exchange_plan (what DeviceReducer hands its Transport) for every
+    rank of a mixed layout: each round's sends and receives pair up one to
+    one with equal sizes (NCCL grouped send/recv matching), the round-1
+    message from r to owner c is r's copy of chunk c, round 2 carries the
+    owner's aggregate, and receive slots never overlap."""
+    rng = np.random.default_rng(nodes)
+    segs, off = [], 0
+    for _ in range(9):
+        n = int(rng.integers(1, 40_000))
+        if rng.random() < 0.3:
+            segs.append(g.Segment(off, n, g.CodecMode.uncompressed, 0, 0))
+        else:
+            segs.append(g.Segment(off, n, g.CodecMode.quantize, int(rng.integers(1, 9)),
+                                  int(rng.choice([32, 64, 128, 512, 100]))))
+        off += n
+    d = off
+    plans = [g.sra_exchange_plan(d, nodes, me, segs) for me in range(nodes)]
+    L = g.sra_layout(d, nodes, segs)
+    msg = L["msg_bytes"]
+    for rnd in range(2):
+        sends = {(me, p): (reg, o, n) for me in range(nodes)
+                 for p, reg, o, n in plans[me]["rounds"][rnd]["sends"]}
+        recvs = {(src, me): (reg, o, n) for me in range(nodes)
+                 for src, reg, o, n in plans[me]["rounds"][rnd]["recvs"]}
+        assert set(sends) == set(recvs)
+        for (a, b), (reg, o, n) in sends.items():
+            assert recvs[(a, b)][2] == n
+            owner = b if rnd == 0 else a
+            assert n == msg[owner]
+            assert reg == ("send" if rnd == 0 else "gather")
+            assert o == plans[a]["gather_offset"][owner]
+        for me in range(nodes):
+            slots = sorted(o for _, reg, o, _ in plans[me]["rounds"][0]["recvs"])
+            assert all(reg == "recv" for _, reg, _, _ in plans[me]["rounds"][0]["recvs"])
+            stride = plans[me]["recv_stride"]
+            assert slots == [k * stride for k in range(len(slots))]
+            assert stride >= msg[me]
