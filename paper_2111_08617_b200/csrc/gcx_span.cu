@@ -1,0 +1,650 @@
+// gcx_span.cu — K1 "span" kernel: single-vector quantize (codec::quantize,
+// /root/reference/proj/src/codec.cpp:24-69) for buckets of 32, 64 and 128,
+// the configuration of C1 and of every default plan (model.hpp default 4/128).
+//
+// Work decomposition: a WARP owns a tile of 4096 consecutive elements and a
+// LANE owns a span (row) of 128 consecutive elements of it (one bucket of 128,
+// two of 64, four of 32), so both passes of the reference algorithm are
+// lane-local:
+//   pass 1  the sequential FP64 sum of squares of each bucket (codec.cpp:41-48)
+//           over the lane's row, in index order (RN(sq + v*v) == fma(v,v,sq):
+//           the square of a float is exact in FP64);
+//   pass 2  level + stochastic rounding + sign of every element
+//           (codec.cpp:50-64) and LSB-first packing into (bits+1)-bit fields
+//           (codec.cpp:97-124): a row is 4 whole 32-element groups and a group
+//           owns exactly W = bits+1 whole 32-bit words, so the fields are
+//           shifted into registers at compile-time positions.
+//
+// Data movement (Blackwell-native).  The tile is staged as 4 QUARTERS (element
+// columns [32g, 32g+32) of all 32 rows); each quarter is ONE 2-D TMA tensor
+// copy (box 32 x 32 floats, rows 512 B apart in HBM, UTMALDG) into a 4 KB
+// shared slot with the 128-byte swizzle, so the lane-per-row LDS.128 reads of
+// both passes are bank-conflict free.  Each warp cycles 5 slots: the slot of
+// group g is refilled with the next quarter as soon as group g is quantized,
+// so the next tile streams in one group ahead and pass 1 of a tile waits only
+// on quarters issued a group earlier.  Completion is counted on one mbarrier
+// per slot.  The packed words of a tile are written to a shared buffer and
+// leave with one bulk store (cp.async.bulk global <- shared).  Key prefixes
+// T(i) (gcx_make_prefix) are laid out per tile as [quad][lane][4] high words
+// then low words, so each lane's next four keys are one coalesced 16-byte load
+// per word half; they ride one group ahead in registers.
+//
+// Bit-exactness: the arithmetic is gcx_device.cuh's.  The
+// FP32 -> FP64 conversion is cvt (exact for zeros and subnormals), so the fast
+// path covers every finite input; a bucket holding a non-finite input (its
+// FP64 sum is then non-finite) and a group with an ambiguous key compare
+// (probability ~3 * 2^-32 per element) are recomputed by the exact
+// per-element path (quantize_field on the full 64-bit key).  The ragged last
+// tile is staged zero-filled (zeros add nothing to a norm and quantize to 0).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "gcx.h"
+#include "gcx_device.cuh"
+#include "gcx_span.h"
+
+namespace gcx_span {
+
+using namespace gcx_dev;
+
+constexpr uint32_t kSpan = 128;          // elements per lane row
+constexpr uint32_t kWTile = 32 * kSpan;  // elements per warp tile
+constexpr uint32_t kSlots = 5;           // quarter slots per warp (4 KB each)
+constexpr uint32_t kSlotFloats = 32 * 32;
+#ifndef GCX_SPAN_WARPS
+#define GCX_SPAN_WARPS 4
+#endif
+constexpr int kWarps = GCX_SPAN_WARPS;
+
+// per-warp shared memory: kSlots swizzled quarter slots, the packed output
+// words of one tile (128 groups x W words), kSlots mbarriers; 1 KB aligned
+// (the 128-byte swizzle pattern repeats every 1024 bytes)
+__host__ __device__ constexpr uint32_t out_words(uint32_t W) { return 128u * W; }
+__host__ __device__ constexpr uint32_t warp_smem_bytes(uint32_t W) {
+  return (kSlots * kSlotFloats * 4 + out_words(W) * 4 + kSlots * 8 + 1023) & ~1023u;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "SPAN_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra SPAN_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 2-D TMA tensor copy global -> shared (UTMALDG), completion on `bar`
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// bulk copy shared -> global (bulk-group completion)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__host__ __device__ __forceinline__ uint64_t mix64h(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// Element e (0..31) of row r in a swizzled quarter slot: the 16-byte chunk
+// e/4 of the row's 128 bytes sits at chunk (e/4) ^ (r % 8) (TMA SWIZZLE_128B).
+__device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t e) {
+  return r * 32u + ((((e >> 2) ^ (r & 7u)) << 2) | (e & 3u));
+}
+
+// a lane's row of the tile: its 4 quarter slots and the row index
+struct RowView {
+  const float* slot[4];
+  uint32_t r;
+  __device__ __forceinline__ float at(uint32_t e) const { return slot[e >> 5][swz(r, e & 31u)]; }
+};
+
+// One element of codec::quantize on the fast path (finite v in a bucket with
+// a non-zero norm).  As quantize_field32 (gcx_device.cuh) with two changes:
+//  * no clamp: norm >= |v| makes a <= 1 and x <= s, and x == s exactly gives
+//    fl == 0, so the key never rounds past s;
+//  * `h` is the key's top word BEFORE the final `z ^= z >> 31` of mix64
+//    (util.hpp:18): the true top word K = h ^ (h >> 31) differs from h by at
+//    most 1, so K < fl <=> h < fl whenever h is not within 1 of fl; those
+//    elements (mn <= 2 after the group) take the exact path.
+// The FP32 -> FP64 conversion is exact for zeros and subnormals: a zero gives
+// x = 0, fl = 0, level 0, never rounded up; the sign is signbit(v) (-0.0 -> 1).
+template <uint32_t BITS>
+__device__ __forceinline__ uint32_t span_field(uint32_t u, double nd, double y, uint32_t h,
+                                               uint32_t& mn) {
+  constexpr double S2 = double((1u << BITS) - 1) * 4294967296.0;
+  const double av = fabs(double(__uint_as_float(u)));
+  const double q0 = __dmul_rn(av, y);
+  const double r = __fma_rn(-nd, q0, av);
+  const double a = __fma_rn(r, y, q0);
+  const double X = __dmul_rn(a, S2);
+  const double T = __dadd_rz(X, 4503599627370496.0);
+  const uint32_t fl = uint32_t(__double2loint(T));
+  const uint32_t lv = uint32_t(__double2hiint(T)) - 0x43300000u;
+  mn = min(mn, h - fl + 1u);
+  const uint32_t l = lv + (h < fl ? 1u : 0u);
+  return l | ((u >> 31) << BITS);
+}
+
+// top word of mix64(seed ^ T) before the final xorshift (see span_field)
+__device__ __forceinline__ uint32_t key_hraw_from_prefix(uint32_t lo, uint32_t hi, uint32_t s_lo,
+                                                         uint32_t s_hi, const HashK& k) {
+  lo ^= s_lo;
+  hi ^= s_hi;
+  asm("add.cc.u32 %0, %0, 0x7f4a7c15;\n\taddc.u32 %1, %1, 0x9e3779b9;" : "+r"(lo), "+r"(hi));
+  xorshift_v<GCX_HASH_HV>(lo, hi, GCX_HASH_HV == 1 ? 30u : k.k30, k.m30);
+  mul64c(lo, hi, 0x1ce4e5b9u, 0xbf58476du);
+  xorshift_v<GCX_HASH_HV>(lo, hi, GCX_HASH_HV == 1 ? 27u : k.k27, k.m27);
+  return __umulhi(lo, 0x133111ebu) + lo * 0x94d049bbu + hi * 0x133111ebu;
+}
+
+__device__ __forceinline__ uint32_t key_hraw_inline(uint32_t i, uint32_t b, uint32_t s_lo,
+                                                    uint32_t s_hi, const HashK& k) {
+  uint32_t lo, hi;
+  draw_prefix<GCX_HASH_HV>(i, b, k, lo, hi);
+  return key_hraw_from_prefix(lo, hi, s_lo, s_hi, k);
+}
+
+template <uint32_t W>
+__device__ __forceinline__ void put_field(uint32_t (&w)[W], uint32_t j, uint32_t f) {
+  const uint32_t bit = j * W, m = bit >> 5, sh = bit & 31u;
+  w[m] |= f << sh;
+  if (sh + W > 32) w[m + 1] |= f >> (32 - sh);
+}
+
+// exact per-element path for group g of a lane's row (any inputs); writes the
+// group's W words to w.  Keys: prefix table words of the tile (hi at
+// ph[quad*128 + lane*4 + k], lo 4096 words later) or inline hashing.
+template <uint32_t BITS, int LGB, bool PREFIX>
+__device__ __noinline__ void span_group_exact(RowView rv, uint32_t g, uint32_t i0, uint32_t nu,
+                                              uint64_t seed, const uint32_t* ph, uint32_t lane,
+                                              uint32_t* w) {
+  constexpr uint32_t W = BITS + 1, S = (1u << BITS) - 1;
+  uint32_t acc[W];
+  for (uint32_t m = 0; m < W; ++m) acc[m] = 0u;
+  if (nu != 0u) {  // all-zero bucket: every field 0, sign too (codec.cpp:50)
+    const Opq opq = make_opq();
+    const double nd = f32abs_to_f64(nu);
+    const double y = __drcp_rn(nd);
+    for (uint32_t j = 0; j < 32; ++j) {
+      uint32_t hl, hh;
+      if (PREFIX) {
+        const uint32_t pos = (g * 8 + (j >> 2)) * 128u + lane * 4u + (j & 3u);
+        const uint64_t z = (uint64_t(ph[pos]) << 32 | ph[pos + 4096]) ^ seed;
+        const uint64_t h = mix64h(z);
+        hl = uint32_t(h);
+        hh = uint32_t(h >> 32);
+      } else {
+        const uint32_t i = i0 + j;
+        draw_key(i, 0u, i >> LGB, 0u, uint32_t(seed), uint32_t(seed >> 32), opq, hl, hh);
+      }
+      const uint32_t f = quantize_field(__float_as_uint(rv.at(g * 32 + j)), nd, y, double(S), S,
+                                        int(BITS), hl, hh);
+      const uint32_t bit = j * W, m = bit >> 5, sh = bit & 31u;
+      acc[m] |= f << sh;
+      if (sh + W > 32) acc[m + 1] |= f >> (32 - sh);
+    }
+  }
+  for (uint32_t m = 0; m < W; ++m) w[m] = acc[m];
+}
+
+// exact sequential norm of elements [e0, e0+cnt) of a row (any inputs) +
+// first non-finite index (codec.cpp:41-48, :43-45)
+__device__ __noinline__ uint32_t span_norm_exact(RowView rv, uint32_t e0, uint32_t cnt, uint32_t i0,
+                                                 unsigned long long* bad) {
+  double sq = 0.0;
+  uint32_t first_bad = ~0u;
+  for (uint32_t j = 0; j < cnt; ++j) {
+    const uint32_t ua = __float_as_uint(rv.at(e0 + j)) & 0x7FFFFFFFu;
+    if (ua >= 0x7F800000u && first_bad == ~0u) first_bad = j;
+    const double d = f32abs_to_f64_nb(ua);
+    sq = __fma_rn(d, d, sq);
+  }
+  if (first_bad != ~0u && bad != nullptr) atomicMin(bad, (unsigned long long)(i0 + first_bad));
+  return __float_as_uint(__double2float_rn(__dsqrt_rn(sq)));
+}
+
+struct SpanArgs {
+  const float* x;
+  uint32_t n;
+  uint32_t nfull;  // full warp tiles
+  uint64_t seed;
+  const uint32_t* prefix;  // span-layout prefix table (words) or nullptr
+  float* norms;
+  uint32_t* packed;
+  unsigned long long* bad;
+  bool tma;     // x 16-byte aligned and the tensor map describes its full rows
+  bool p_al16;  // packed 16-byte aligned: bulk store
+};
+
+__device__ __forceinline__ uint4 ldg_nc_v4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 lds_v4(const float* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+
+// pass 2 of one group on the fast path; returns false when the group needs the
+// exact path (ambiguous key compare).  Keys ride one group ahead in a ring of
+// 8 quads: the group's 32 key words are hashed first, then the next group's
+// keys (kn, or nothing when kn == nullptr) are loaded into the ring, then the
+// elements are quantized — the loads are volatile so they stay ahead of the
+// shared-memory reads and get a whole group of work to land.
+template <uint32_t BITS, int LGB, bool PREFIX>
+__device__ __forceinline__ bool span_group_fast(const float* slot, uint32_t lane, uint32_t i0,
+                                                uint32_t nu, uint32_t s_lo, uint32_t s_hi,
+                                                const HashK& shk, uint32_t (&w)[BITS + 1],
+                                                uint4 (&kh)[8], uint4 (&kl)[8], const uint4* kn) {
+  constexpr uint32_t W = BITS + 1;
+  const uint32_t b = i0 >> LGB;
+  const float* row = slot + lane * 32u;
+  const uint32_t key = lane & 7u;
+  uint32_t hh[32];
+  if (PREFIX) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      hh[4 * q + 0] = key_hraw_from_prefix(kl[q].x, kh[q].x, s_lo, s_hi, shk);
+      hh[4 * q + 1] = key_hraw_from_prefix(kl[q].y, kh[q].y, s_lo, s_hi, shk);
+      hh[4 * q + 2] = key_hraw_from_prefix(kl[q].z, kh[q].z, s_lo, s_hi, shk);
+      hh[4 * q + 3] = key_hraw_from_prefix(kl[q].w, kh[q].w, s_lo, s_hi, shk);
+    }
+    if (kn != nullptr) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        kh[q] = ldg_nc_v4(kn + q * 32);
+        kl[q] = ldg_nc_v4(kn + 1024 + q * 32);
+      }
+    }
+  }
+  const double nd = f32abs_to_f64(nu);
+  const double y = __drcp_rn(nd);
+  uint32_t mn = ~0u;
+#pragma unroll
+  for (int m = 0; m < int(W); ++m) w[m] = 0u;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 v = lds_v4(row + ((uint32_t(q) ^ key) << 2));
+    const uint32_t u[4] = {__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z),
+                           __float_as_uint(v.w)};
+    if (!PREFIX) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) hh[4 * q + k] = key_hraw_inline(i0 + 4 * q + k, b, s_lo, s_hi, shk);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      put_field<W>(w, uint32_t(4 * q + k), span_field<BITS>(u[k], nd, y, hh[4 * q + k], mn));
+  }
+  return mn > 2u;
+}
+
+template <uint32_t BITS, int LGB, bool PREFIX>
+__global__ void __launch_bounds__(32 * kWarps, 1)
+    k_span(const __grid_constant__ CUtensorMap tmap, SpanArgs A) {
+  constexpr uint32_t W = BITS + 1;
+  constexpr uint32_t BL = 1u << LGB;  // bucket length
+  constexpr uint32_t NB = kSpan / BL;  // buckets per row (1, 2, 4)
+  constexpr uint32_t GPB = BL / 32;    // groups per bucket (4, 2, 1)
+  extern __shared__ __align__(1024) unsigned char span_smem[];
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  unsigned char* base = span_smem + warp * warp_smem_bytes(W);
+  float* slots = reinterpret_cast<float*>(base);
+  uint32_t* outw = reinterpret_cast<uint32_t*>(base + kSlots * kSlotFloats * 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + kSlots * kSlotFloats * 4 + out_words(W) * 4);
+  const uint32_t gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+  const uint32_t ntiles = A.nfull + (A.n > A.nfull * kWTile ? 1u : 0u);
+  const HashK shk = make_hashk();
+  const uint32_t s_lo = uint32_t(A.seed), s_hi = uint32_t(A.seed >> 32);
+
+  if (lane == 0) {
+    for (uint32_t s = 0; s < kSlots; ++s) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  // Quarter Q of this warp's work = quarter Q % 4 of its (Q / 4)-th tile; it
+  // lives in slot Q % 5, whose mbarrier completes its (Q / 5)-th phase.
+  auto issue = [&](uint32_t Q) {
+    const uint32_t t = gw + (Q >> 2) * nw, g = Q & 3u;
+    if (t >= ntiles) return;
+    const uint32_t s = Q % kSlots;
+    float* dst = slots + s * kSlotFloats;
+    if (A.tma && t < A.nfull) {
+      if (lane == 0) {
+        fence_async_smem();  // this slot's generic reads precede the async write
+        mbar_arrive_expect_tx(bars + s, kSlotFloats * 4);
+        tma_load_2d(dst, &tmap, int32_t(g * 32), int32_t(t * 32), bars + s);
+      }
+    } else {  // unaligned input or the ragged last tile: zero-filled register copy
+      const uint64_t t0 = uint64_t(t) * kWTile;
+      for (uint32_t r = 0; r < 32; ++r) {
+        const uint64_t i = t0 + r * kSpan + g * 32 + lane;
+        dst[swz(r, lane)] = i < A.n ? A.x[i] : 0.0f;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bars + s);
+    }
+  };
+  auto wait_q = [&](uint32_t Q) { mbar_wait(bars + Q % kSlots, (Q / kSlots) & 1u); };
+
+  uint4 kh[8], kl[8];
+  if (PREFIX && gw < ntiles) {
+    const uint4* k0 = reinterpret_cast<const uint4*>(A.prefix + uint64_t(gw) * 8192u) + lane;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      kh[q] = __ldg(k0 + q * 32);
+      kl[q] = __ldg(k0 + 1024 + q * 32);
+    }
+  }
+  for (uint32_t Q = 0; Q < kSlots; ++Q) issue(Q);
+
+  uint32_t j = 0;
+  for (uint32_t t = gw; t < ntiles; t += nw, ++j) {
+    const bool more = t + nw < ntiles;
+    const bool full = t < A.nfull;
+    const uint32_t i_lane = t * kWTile + lane * kSpan;  // first element of the row
+    RowView rv;
+#pragma unroll
+    for (uint32_t g = 0; g < 4; ++g) rv.slot[g] = slots + ((4 * j + g) % kSlots) * kSlotFloats;
+    rv.r = lane;
+
+    // ---- pass 1: sequential FP64 norms of the row's buckets, quarter by quarter ----
+    uint32_t nu[NB];
+    bool careful[NB];
+    {
+      double sq = 0.0;
+#pragma unroll
+      for (uint32_t g = 0; g < 4; ++g) {
+        wait_q(4 * j + g);
+        const float* row = rv.slot[g] + lane * 32u;
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q) {
+          const float4 v = *reinterpret_cast<const float4*>(row + ((q ^ (lane & 7u)) << 2));
+          // exact conversion for every finite float; a non-finite input makes
+          // sq non-finite (squares of floats cannot overflow FP64)
+          double d = double(v.x);
+          sq = __fma_rn(d, d, sq);
+          d = double(v.y);
+          sq = __fma_rn(d, d, sq);
+          d = double(v.z);
+          sq = __fma_rn(d, d, sq);
+          d = double(v.w);
+          sq = __fma_rn(d, d, sq);
+        }
+        if ((g * 32 + 32) % BL == 0) {  // bucket r complete
+          const uint32_t r = (g * 32) / BL;
+          const bool c = (uint32_t(__double2hiint(sq)) & 0x7FF00000u) == 0x7FF00000u;
+          const uint32_t v = c ? span_norm_exact(rv, r * BL, BL, i_lane + r * BL, A.bad)
+                               : __float_as_uint(__double2float_rn(__dsqrt_rn(sq)));
+#pragma unroll
+          for (uint32_t rr = 0; rr < NB; ++rr)
+            if (rr == r) {
+              nu[rr] = v;
+              careful[rr] = c;
+            }
+          if (full || i_lane + r * BL < A.n) A.norms[(i_lane >> LGB) + r] = __uint_as_float(v);
+          sq = 0.0;
+        }
+      }
+    }
+
+    // ---- pass 2: quantize + pack the row's 4 groups ----
+    if (A.p_al16 && lane == 0) bulk_wait_read0();  // previous tile's bulk store has read outw
+    __syncwarp();
+    // key ring: group 0 of this tile was loaded during the previous tile (or
+    // before the loop); group g+1 (or group 0 of the next tile) loads during g
+    const uint4* kp = PREFIX ? reinterpret_cast<const uint4*>(A.prefix + uint64_t(t) * 8192u) + lane
+                             : nullptr;
+    const uint4* kp_next =
+        PREFIX && more ? reinterpret_cast<const uint4*>(A.prefix + uint64_t(t + nw) * 8192u) + lane
+                       : nullptr;
+#pragma unroll 1
+    for (uint32_t g = 0; g < 4; ++g) {
+      const uint32_t r = g / GPB;
+      uint32_t nug = nu[0];
+      bool car = careful[0];
+#pragma unroll
+      for (uint32_t rr = 1; rr < NB; ++rr)
+        if (r == rr) {
+          nug = nu[rr];
+          car = careful[rr];
+        }
+      const uint32_t i0 = i_lane + g * 32;
+      const uint4* kn = g < 3 ? kp + (g + 1) * 256 : kp_next;
+      if (PREFIX && lane == 0) {  // keys two groups ahead into L2 (the ring loads then hit L2)
+        const uint4* k2 = g < 2 ? kp + (g + 2) * 256 : (kp_next ? kp_next + (g - 2) * 256 : nullptr);
+        if (k2 != nullptr) {
+          prefetch_l2(k2 - lane, 4096);
+          prefetch_l2(k2 - lane + 1024, 4096);
+        }
+      }
+      const float* slot = slots + ((4 * j + g) % kSlots) * kSlotFloats;
+      // The fast path always runs (its result is discarded for an all-zero or
+      // non-finite bucket), so the key ring flows through one code path; the
+      // exact path writes its words itself, so no local-memory result merges
+      // into registers the key-ring loads are pending on.
+      uint32_t* wout = outw + (lane * 4 + g) * W;
+      uint32_t w[W];
+      const bool ok = span_group_fast<BITS, LGB, PREFIX>(slot, lane, i0, nug, s_lo, s_hi, shk, w, kh,
+                                                         kl, kn) &&
+                      nug != 0u && !car;
+      if (ok) {
+#pragma unroll
+        for (int m = 0; m < int(W); ++m) wout[m] = w[m];
+      } else {
+        span_group_exact<BITS, LGB, PREFIX>(rv, g, i0, nug, A.seed,
+                                            PREFIX ? A.prefix + uint64_t(t) * 8192u : nullptr, lane,
+                                            wout);
+      }
+      __syncwarp();               // every lane is done with this slot
+      issue(4 * j + g + kSlots);  // refill it: the quarter kSlots ahead
+    }
+    __syncwarp();
+    uint32_t* dstw = A.packed + uint64_t(t) * out_words(W);
+    if (A.p_al16 && full) {
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) bulk_s2g(dstw, outw, out_words(W) * 4);
+    } else {  // only the words the vector owns (gcx_packed_capacity)
+      const uint32_t nwords =
+          full ? out_words(W) : uint32_t((uint64_t(A.n - t * kWTile) * W + 31) / 32);
+      for (uint32_t e = lane; e < nwords; e += 32) dstw[e] = outw[e];
+    }
+    __syncwarp();  // outw free for reuse
+  }
+  if (A.p_al16 && lane == 0) bulk_wait0();  // bulk stores complete before exit
+}
+
+// Prefix table in span layout: per tile of 4096 elements, 4096 high words
+// ordered [quad][lane][4] then the 4096 low words; slot of element
+// e = tile*4096 + lane*128 + 4q + k is hi[q*128 + lane*4 + k].
+// T(i) = mix64((i >> lgb) ^ mix64(i)) (util.hpp:26-29 without the seed).
+__global__ void __launch_bounds__(256) k_span_prefix(uint32_t n, uint32_t lgb, uint32_t ntiles,
+                                                     uint4* __restrict__ table) {
+  const uint64_t total = uint64_t(ntiles) * 1024u;
+  for (uint64_t u = blockIdx.x * 256ull + threadIdx.x; u < total; u += uint64_t(gridDim.x) * 256u) {
+    const uint32_t tile = uint32_t(u >> 10), w = uint32_t(u & 1023u);
+    const uint32_t q = w >> 5, lane = w & 31u;
+    const uint32_t e0 = tile * kWTile + lane * kSpan + q * 4;
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t i = e0 + k;
+      const uint64_t z = i < n ? mix64h(uint64_t(i >> lgb) ^ mix64h(uint64_t(i))) : 0ull;
+      hi[k] = uint32_t(z >> 32);
+      lo[k] = uint32_t(z);
+    }
+    table[uint64_t(tile) * 2048 + w] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    table[uint64_t(tile) * 2048 + 1024 + w] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
+using SpanFn = void (*)(const __grid_constant__ CUtensorMap, SpanArgs);
+
+template <uint32_t BITS>
+SpanFn pick_lgb(int lgb, bool prefix) {
+  switch (lgb) {
+    case 5: return prefix ? k_span<BITS, 5, true> : k_span<BITS, 5, false>;
+    case 6: return prefix ? k_span<BITS, 6, true> : k_span<BITS, 6, false>;
+    case 7: return prefix ? k_span<BITS, 7, true> : k_span<BITS, 7, false>;
+    default: return nullptr;
+  }
+}
+
+SpanFn pick(int bits, int lgb, bool prefix) {
+  switch (bits) {
+    case 1: return pick_lgb<1>(lgb, prefix);
+    case 2: return pick_lgb<2>(lgb, prefix);
+    case 3: return pick_lgb<3>(lgb, prefix);
+    case 4: return pick_lgb<4>(lgb, prefix);
+    case 5: return pick_lgb<5>(lgb, prefix);
+    case 6: return pick_lgb<6>(lgb, prefix);
+    case 7: return pick_lgb<7>(lgb, prefix);
+    case 8: return pick_lgb<8>(lgb, prefix);
+    default: return nullptr;
+  }
+}
+
+int lgb_of(uint64_t bucket) {
+  return bucket == 32 ? 5 : bucket == 64 ? 6 : bucket == 128 ? 7 : -1;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// The vector's full 128-element rows as a 2-D tensor {128, rows}; box {32, 32}
+// = one quarter of a warp tile, 128-byte swizzle.
+bool make_tmap(const float* x, uint64_t rows, CUtensorMap* map) {
+  EncodeFn fn = encode_fn();
+  if (fn == nullptr || rows == 0) return false;
+  const cuuint64_t dims[2] = {kSpan, rows};
+  const cuuint64_t strides[1] = {kSpan * 4};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace gcx_span
+
+using namespace gcx_span;
+
+bool gcx_span_supported(uint64_t bucket) { return lgb_of(bucket) > 0; }
+
+uint64_t gcx_span_prefix_slots(uint64_t n) { return (n + kWTile - 1) / kWTile * kWTile; }
+
+cudaError_t gcx_span_make_prefix(uint64_t n, uint64_t bucket, unsigned long long* table,
+                                 int sms, cudaStream_t st) {
+  const int lgb = lgb_of(bucket);
+  if (lgb < 0) return cudaErrorInvalidValue;
+  const uint32_t ntiles = uint32_t((n + kWTile - 1) / kWTile);
+  const uint64_t threads = uint64_t(ntiles) * 1024u;
+  const uint64_t blocks = (threads + 255) / 256;
+  const uint32_t grid = uint32_t(blocks < uint64_t(sms) * 8 ? blocks : uint64_t(sms) * 8);
+  k_span_prefix<<<grid > 0 ? grid : 1, 256, 0, st>>>(uint32_t(n), uint32_t(lgb), ntiles,
+                                                      reinterpret_cast<uint4*>(table));
+  return cudaGetLastError();
+}
+
+cudaError_t gcx_span_quantize(const float* x, uint64_t n, int bits, uint64_t bucket, uint64_t seed,
+                              const unsigned long long* prefix, float* norms, uint8_t* packed,
+                              unsigned long long* bad, int sms, cudaStream_t st) {
+  const int lgb = lgb_of(bucket);
+  SpanFn fn = pick(bits, lgb, prefix != nullptr);
+  if (fn == nullptr) return cudaErrorInvalidValue;
+  const uint32_t W = uint32_t(bits) + 1;
+  const size_t smem = size_t(kWarps) * warp_smem_bytes(W);
+  static thread_local int occ[9][8][2] = {};
+  int& o = occ[bits][lgb][prefix != nullptr];
+  if (o == 0) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 32 * kWarps, smem);
+    if (e != cudaSuccess) return e;
+    if (o < 1) o = 1;
+  }
+  SpanArgs a;
+  a.x = x;
+  a.n = uint32_t(n);
+  a.nfull = uint32_t(n / kWTile);
+  a.seed = seed;
+  a.prefix = reinterpret_cast<const uint32_t*>(prefix);
+  a.norms = norms;
+  a.packed = reinterpret_cast<uint32_t*>(packed);
+  a.bad = bad;
+  a.p_al16 = (reinterpret_cast<uintptr_t>(packed) & 15u) == 0;
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  a.tma = (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && a.nfull > 0 &&
+          make_tmap(x, uint64_t(a.nfull) * 32, &map);
+  const uint32_t tiles = uint32_t((n + kWTile - 1) / kWTile);
+  uint32_t grid = (tiles + kWarps - 1) / kWarps;
+  if (grid > uint32_t(sms * o)) grid = uint32_t(sms * o);
+  if (grid == 0) grid = 1;
+  fn<<<grid, 32 * kWarps, smem, st>>>(map, a);
+  return cudaGetLastError();
+}

@@ -1,0 +1,17 @@
+// gcx_span.h — internal interface of the span K1 kernel (gcx_span.cu) used by
+// the C-ABI in gcx_kernels.cu.  Not part of the public boundary (include/gcx.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+// buckets the span kernel handles (32, 64, 128)
+bool gcx_span_supported(uint64_t bucket);
+// prefix-table slots (8 bytes each) of an n-element vector in span layout
+uint64_t gcx_span_prefix_slots(uint64_t n);
+cudaError_t gcx_span_make_prefix(uint64_t n, uint64_t bucket, unsigned long long* table, int sms,
+                                 cudaStream_t st);
+// prefix == nullptr: keys hashed inline (three SplitMix64 finalizers)
+cudaError_t gcx_span_quantize(const float* x, uint64_t n, int bits, uint64_t bucket, uint64_t seed,
+                              const unsigned long long* prefix, float* norms, uint8_t* packed,
+                              unsigned long long* bad, int sms, cudaStream_t st);
