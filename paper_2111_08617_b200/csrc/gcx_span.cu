@@ -40,6 +40,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 
@@ -526,6 +527,143 @@ __global__ void __launch_bounds__(256) k_span_prefix(uint32_t n, uint32_t lgb, u
   }
 }
 
+// ---------------------------------------------------------------------------
+// K3 span decode (codec::dequantize, codec.cpp:71-95, + finalize's average,
+// collectives.cpp:213-228) for bits <= 4 and power-of-two buckets of 128 ..
+// 4096 (C1 and the default plans).  A warp owns a tile of 4096 elements = 32
+// chunks of 128; every chunk lies in one bucket, so the chunk's signed
+// dequantization table has F = 2^(bits+1) <= 32 entries and lives one entry
+// per LANE: lane k computes entry f = k % F once per chunk (one FP64 RN(norm *
+// level / s) per lane, bit-exact as dequant_field), and each element's value
+// is one warp shuffle from the lane holding its field.  No shared-memory
+// table, no bank conflicts.  Lane l decodes elements 4l..4l+3 of each chunk
+// (its 4W-bit window of the chunk's packed words, staged per tile in shared
+// memory by coalesced 16-byte loads) and writes them with one coalesced
+// 16-byte streaming store: the kernel moves C(n) + 4n bytes and little else.
+// ---------------------------------------------------------------------------
+constexpr int kDWarps = 8;
+#ifndef GCX_DSPAN_MINB
+#define GCX_DSPAN_MINB 4
+#endif
+
+struct DspanArgs {
+  const float* norms;
+  const uint32_t* packed;
+  float* out;
+  uint32_t n;
+  float div, recip;
+  bool pow2;
+};
+
+template <uint32_t BITS, uint32_t LGB>
+__global__ void __launch_bounds__(32 * kDWarps, GCX_DSPAN_MINB) k_dspan(DspanArgs A) {
+  constexpr uint32_t W = BITS + 1, S = (1u << BITS) - 1, F = 2u << BITS;
+  constexpr uint32_t TW = 128u * W;               // packed words per tile
+  constexpr uint32_t NBT = kWTile >> LGB;         // buckets per tile (1..32)
+  constexpr uint32_t BSH = LGB - 7;               // chunks per bucket = 2^BSH
+  __shared__ __align__(16) uint32_t words_all[kDWarps][TW];
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t* words = words_all[warp];
+  const uint32_t gw = blockIdx.x * kDWarps + warp, nw = gridDim.x * kDWarps;
+  const uint32_t ntiles = (A.n + kWTile - 1) / kWTile;
+  const uint32_t nwords = uint32_t((uint64_t(A.n) * W + 31) / 32);  // gcx_packed_capacity / 4
+  const uint32_t nbk = (A.n + (1u << LGB) - 1) >> LGB;
+  // this lane's table entry: field f = level | sign << BITS
+  const uint32_t f = lane & (F - 1u), level = f & S, sign = f >> BITS;
+  const double dl = double(level);
+  const double sd = double(S), ys = __drcp_rn(sd);
+  // this lane's 4W-bit window inside every chunk
+  const uint32_t qbit = 4 * W * lane, qw = qbit >> 5, qsh = qbit & 31u;
+  const bool two = qsh + 4 * W > 32;
+  for (uint32_t t = gw; t < ntiles; t += nw) {
+    const uint32_t e0 = t * kWTile;
+    const bool full = e0 + kWTile <= A.n;
+    // stage the tile's packed words (coalesced 16-byte loads) and its norms
+    const uint32_t* src = A.packed + uint64_t(t) * TW;
+    const uint32_t b0 = e0 >> LGB;
+    const uint32_t nreg =
+        lane < NBT && b0 + lane < nbk ? __ldg(reinterpret_cast<const uint32_t*>(A.norms) + b0 + lane) : 0u;
+    if (full) {
+      uint4 st[W];
+#pragma unroll
+      for (uint32_t k = 0; k < W; ++k) st[k] = __ldcs(reinterpret_cast<const uint4*>(src) + k * 32 + lane);
+#pragma unroll
+      for (uint32_t k = 0; k < W; ++k) reinterpret_cast<uint4*>(words)[k * 32 + lane] = st[k];
+    } else {
+      for (uint32_t k = lane; k < TW; k += 32) words[k] = t * TW + k < nwords ? src[k] : 0u;
+    }
+    __syncwarp();
+    float* out = A.out + e0 + 4 * lane;
+    const bool vec = (reinterpret_cast<uintptr_t>(out) & 15u) == 0 && full;
+    // batches of 8 chunks: the batch's table entries (one per bucket it
+    // touches: RN32(RN64(RN64(norm * level) / s)), /N, signed) are 1..8
+    // independent FP64 chains, then the chunks are decoded by shuffles
+    constexpr uint32_t CB = 8;
+    constexpr uint32_t NEB = (CB >> BSH) > 0 ? (CB >> BSH) : 1;
+#pragma unroll
+    for (uint32_t bb = 0; bb < 32 / CB; ++bb) {
+      if (!full && e0 + bb * CB * 128 >= A.n) break;
+      float entry[NEB];
+#pragma unroll
+      for (uint32_t i = 0; i < NEB; ++i) {
+        const uint32_t nu = __shfl_sync(0xffffffffu, nreg, ((bb * CB) >> BSH) + i);
+        const double nl = __dmul_rn(double(__uint_as_float(nu)), dl);  // exact
+        const double q0 = __dmul_rn(nl, ys);
+        const double q = __fma_rn(__fma_rn(-sd, q0, nl), ys, q0);  // RN(nl / s), see dequant_field
+        const float m = apply_divisor(__double2float_rn(q), A.div, A.recip, A.pow2);
+        entry[i] = level == 0 ? 0.0f : (sign ? -m : m);
+      }
+#pragma unroll
+      for (uint32_t cc = 0; cc < CB; ++cc) {
+        const uint32_t c = bb * CB + cc;
+        if (!full && e0 + c * 128 >= A.n) break;
+        const uint32_t* cw = words + c * 4 * W + qw;
+        const uint32_t win = two ? __funnelshift_r(cw[0], cw[1], qsh) : (cw[0] >> qsh);
+        const float en = entry[NEB > 1 ? (cc >> BSH) : 0];
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          v[k] = __shfl_sync(0xffffffffu, en, (win >> (k * W)) & (F - 1u));
+        float* o = out + c * 128;
+        if (vec) {
+          __stcs(reinterpret_cast<float4*>(o), make_float4(v[0], v[1], v[2], v[3]));
+        } else {
+          const uint32_t e = e0 + c * 128 + 4 * lane;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (e + k < A.n) __stcs(o + k, v[k]);
+        }
+      }
+    }
+    __syncwarp();  // words[] is restaged by the next tile
+  }
+}
+
+using DspanFn = void (*)(DspanArgs);
+
+template <uint32_t BITS>
+DspanFn pick_dspan_lgb(uint32_t lgb) {
+  switch (lgb) {
+    case 7: return k_dspan<BITS, 7>;
+    case 8: return k_dspan<BITS, 8>;
+    case 9: return k_dspan<BITS, 9>;
+    case 10: return k_dspan<BITS, 10>;
+    case 11: return k_dspan<BITS, 11>;
+    case 12: return k_dspan<BITS, 12>;
+    default: return nullptr;
+  }
+}
+
+DspanFn pick_dspan(int bits, uint32_t lgb) {
+  switch (bits) {
+    case 1: return pick_dspan_lgb<1>(lgb);
+    case 2: return pick_dspan_lgb<2>(lgb);
+    case 3: return pick_dspan_lgb<3>(lgb);
+    case 4: return pick_dspan_lgb<4>(lgb);
+    default: return nullptr;
+  }
+}
+
 using SpanFn = void (*)(const __grid_constant__ CUtensorMap, SpanArgs);
 
 template <uint32_t BITS>
@@ -646,5 +784,42 @@ cudaError_t gcx_span_quantize(const float* x, uint64_t n, int bits, uint64_t buc
   if (grid > uint32_t(sms * o)) grid = uint32_t(sms * o);
   if (grid == 0) grid = 1;
   fn<<<grid, 32 * kWarps, smem, st>>>(map, a);
+  return cudaGetLastError();
+}
+
+bool gcx_span_decode_supported(int bits, uint64_t bucket) {
+  return bits >= 1 && bits <= 4 && bucket >= 128 && bucket <= kWTile && (bucket & (bucket - 1)) == 0;
+}
+
+cudaError_t gcx_span_dequantize(const float* norms, const uint8_t* packed, uint64_t n, int bits,
+                                uint64_t bucket, float* out, float divisor, int sms,
+                                cudaStream_t st) {
+  if (!gcx_span_decode_supported(bits, bucket)) return cudaErrorInvalidValue;
+  if (reinterpret_cast<uintptr_t>(packed) & 15u) return cudaErrorInvalidValue;
+  uint32_t lgb = 0;
+  while ((1ull << lgb) < bucket) ++lgb;
+  DspanFn fn = pick_dspan(bits, lgb);
+  if (fn == nullptr) return cudaErrorInvalidValue;
+  static thread_local int occ[9][13] = {};
+  int& o = occ[bits][lgb];
+  if (o == 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 32 * kDWarps, 0);
+    if (e != cudaSuccess) return e;
+    if (o < 1) o = 1;
+  }
+  DspanArgs a;
+  a.norms = norms;
+  a.packed = reinterpret_cast<const uint32_t*>(packed);
+  a.out = out;
+  a.n = uint32_t(n);
+  a.div = divisor;
+  a.recip = 1.0f / divisor;
+  int e2 = 0;
+  a.pow2 = std::frexp(divisor, &e2) == 0.5f;
+  const uint32_t tiles = uint32_t((n + kWTile - 1) / kWTile);
+  uint32_t grid = (tiles + kDWarps - 1) / kDWarps;
+  if (grid > uint32_t(sms * o)) grid = uint32_t(sms * o);
+  if (grid == 0) grid = 1;
+  fn<<<grid, 32 * kDWarps, 0, st>>>(a);
   return cudaGetLastError();
 }

@@ -15,3 +15,8 @@ cudaError_t gcx_span_make_prefix(uint64_t n, uint64_t bucket, unsigned long long
 cudaError_t gcx_span_quantize(const float* x, uint64_t n, int bits, uint64_t bucket, uint64_t seed,
                               const unsigned long long* prefix, float* norms, uint8_t* packed,
                               unsigned long long* bad, int sms, cudaStream_t st);
+// K3 span decode: bits 1..4, power-of-two buckets 128..4096; packed 16-byte aligned
+bool gcx_span_decode_supported(int bits, uint64_t bucket);
+cudaError_t gcx_span_dequantize(const float* norms, const uint8_t* packed, uint64_t n, int bits,
+                                uint64_t bucket, float* out, float divisor, int sms,
+                                cudaStream_t st);

@@ -148,3 +148,31 @@ def test_span_seeds_differ_only_in_keys(dev, oracle):
         torch.cuda.synchronize()
         wn, wp = oracle.quantize(v, 4, 128, seed)
         assert (packed.cpu().numpy()[: wp.size] == wp).all(), seed
+
+
+@pytest.mark.parametrize("bits", [1, 2, 3, 4])
+@pytest.mark.parametrize("bucket", [128, 256, 512, 1024, 2048, 4096])
+def test_span_decode_vs_oracle(dev, oracle, bits, bucket):
+    """K3 span decode (shuffle tables, one chunk of 128 per bucket slice):
+    bit-exact dequantize (codec.cpp:71-95) over full tiles, a ragged tile and
+    an output pointer that is only 4-byte aligned."""
+    rng = np.random.default_rng(bits * 100 + bucket)
+    for n in (4096 * 11 + int(rng.integers(1, 4096)), 100, 4096, 129):
+        v = (rng.standard_normal(n) * 10.0 ** rng.integers(-20, 20)).astype(np.float32)
+        v[rng.random(n) < 0.01] = np.float32(-0.0)
+        seed = int(rng.integers(0, 2**63))
+        wn, wp = oracle.quantize(v, bits, bucket, seed)
+        want = oracle.dequantize(wn, wp, n, bits, bucket)
+        from paper_2111_08617_b200 import _capi
+        cap = _capi.packed_capacity(n, bits)
+        pk = np.zeros(cap, np.uint8)
+        pk[: wp.size] = wp
+        for off in (0, 1):
+            obuf = torch.full((n + 4,), 7.0, dtype=torch.float32, device="cuda")
+            out = obuf[off:off + n]
+            dev.dequantize(torch.from_numpy(wn).cuda(), torch.from_numpy(pk).cuda(), n, bits, bucket,
+                           out=out)
+            torch.cuda.synchronize()
+            got = obuf.cpu().numpy()
+            assert (got[off:off + n].view(np.uint32) == want.view(np.uint32)).all(), (n, off)
+            assert (got[off + n:] == 7.0).all() and (got[:off] == 7.0).all()
