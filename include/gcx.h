@@ -48,6 +48,8 @@ extern "C" {
 #define GCX_F_NORM_PASS 16u    /* some piece's norms come from the K1a pre-pass (bucket not 32/64/128) */
 #define GCX_F_LANE_GROUP 32u   /* some piece has bucket % 32 == 0 other than 32/64/128 (k_quant32) */
 #define GCX_F_KEY_PREFIX 64u   /* the key table holds seed-independent prefixes (gcx_make_prefix) */
+#define GCX_F_SPAN_DEC 128u    /* every piece is raw or bits<=4 with a power-of-two bucket in
+                                  [128, 4096]: the shuffle-table span decode serves the table */
 
 #define GCX_TILE 4096          /* max elements per CTA tile */
 

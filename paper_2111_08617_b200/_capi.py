@@ -19,6 +19,8 @@ GCX_F_PIECE_SEEDS = 4
 GCX_F_ODD_BUCKETS = 8
 GCX_F_NORM_PASS = 16
 GCX_F_LANE_GROUP = 32
+GCX_F_KEY_PREFIX = 64
+GCX_F_SPAN_DEC = 128
 GCX_TILE = 4096
 
 

@@ -25,9 +25,10 @@
 // on quarters issued a group earlier.  Completion is counted on one mbarrier
 // per slot.  The packed words of a tile are written to a shared buffer and
 // leave with one bulk store (cp.async.bulk global <- shared).  Key prefixes
-// T(i) (gcx_make_prefix) are laid out per tile as [quad][lane][4] high words
-// then low words, so each lane's next four keys are one coalesced 16-byte load
-// per word half; they ride one group ahead in registers.
+// T(i) (gcx_make_prefix) use the span key layout (span_key_pos): per tile and
+// group, 1024 high words ordered [quad][lane][4] then the 1024 low words, so
+// each lane's next four keys are one coalesced 16-byte load per word half;
+// they ride one group ahead in registers.
 //
 // Bit-exactness: the arithmetic is gcx_device.cuh's.  The
 // FP32 -> FP64 conversion is cvt (exact for zeros and subnormals), so the fast
@@ -46,6 +47,7 @@
 
 #include "gcx.h"
 #include "gcx_device.cuh"
+#include "gcx_plan.cuh"
 #include "gcx_span.h"
 
 namespace gcx_span {
@@ -209,9 +211,9 @@ __device__ __noinline__ void span_group_exact(RowView rv, uint32_t g, uint32_t i
     const double y = __drcp_rn(nd);
     for (uint32_t j = 0; j < 32; ++j) {
       uint32_t hl, hh;
-      if (PREFIX) {
-        const uint32_t pos = (g * 8 + (j >> 2)) * 128u + lane * 4u + (j & 3u);
-        const uint64_t z = (uint64_t(ph[pos]) << 32 | ph[pos + 4096]) ^ seed;
+      if (PREFIX) {  // ph: the tile's first key word (span_key_pos)
+        const uint32_t pos = g * 2048u + (j >> 2) * 128u + lane * 4u + (j & 3u);
+        const uint64_t z = (uint64_t(ph[pos]) << 32 | ph[pos + 1024]) ^ seed;
         const uint64_t h = mix64h(z);
         hl = uint32_t(h);
         hh = uint32_t(h >> 32);
@@ -301,7 +303,7 @@ __device__ __forceinline__ bool span_group_fast(const float* slot, uint32_t lane
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         kh[q] = ldg_nc_v4(kn + q * 32);
-        kl[q] = ldg_nc_v4(kn + 1024 + q * 32);
+        kl[q] = ldg_nc_v4(kn + 256 + q * 32);
       }
     }
   }
@@ -381,7 +383,7 @@ __global__ void __launch_bounds__(32 * kWarps, 1)
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       kh[q] = __ldg(k0 + q * 32);
-      kl[q] = __ldg(k0 + 1024 + q * 32);
+      kl[q] = __ldg(k0 + 256 + q * 32);
     }
   }
   for (uint32_t Q = 0; Q < kSlots; ++Q) issue(Q);
@@ -458,13 +460,10 @@ __global__ void __launch_bounds__(32 * kWarps, 1)
           car = careful[rr];
         }
       const uint32_t i0 = i_lane + g * 32;
-      const uint4* kn = g < 3 ? kp + (g + 1) * 256 : kp_next;
+      const uint4* kn = g < 3 ? kp + (g + 1) * 512 : kp_next;
       if (PREFIX && lane == 0) {  // keys two groups ahead into L2 (the ring loads then hit L2)
-        const uint4* k2 = g < 2 ? kp + (g + 2) * 256 : (kp_next ? kp_next + (g - 2) * 256 : nullptr);
-        if (k2 != nullptr) {
-          prefetch_l2(k2 - lane, 4096);
-          prefetch_l2(k2 - lane + 1024, 4096);
-        }
+        const uint4* k2 = g < 2 ? kp + (g + 2) * 512 : (kp_next ? kp_next + (g - 2) * 512 : nullptr);
+        if (k2 != nullptr) prefetch_l2(k2 - lane, 8192);
       }
       const float* slot = slots + ((4 * j + g) % kSlots) * kSlotFloats;
       // The fast path always runs (its result is discarded for an all-zero or
@@ -503,27 +502,41 @@ __global__ void __launch_bounds__(32 * kWarps, 1)
   if (A.p_al16 && lane == 0) bulk_wait0();  // bulk stores complete before exit
 }
 
-// Prefix table in span layout: per tile of 4096 elements, 4096 high words
-// ordered [quad][lane][4] then the 4096 low words; slot of element
-// e = tile*4096 + lane*128 + 4q + k is hi[q*128 + lane*4 + k].
-// T(i) = mix64((i >> lgb) ^ mix64(i)) (util.hpp:26-29 without the seed).
+// Span key layout (prefix and key tables of the span K1 kernels): slot t of
+// a run (runs start on multiples of 4096 slots) = element t of a piece; with
+// tile T = t >> 12, row r = (t >> 7) & 31, quad q = (t >> 2) & 31, k = t & 3,
+// its high word sits in block b = 4T + q/8 (2048 words: 1024 high words, then
+// the 1024 low words) at (q % 8) * 128 + r * 4 + k.  Blocks of 1024 slots with
+// high words first are also the lane-group layout's (key_pos), so slot-wise
+// passes (gcx_make_keys_prefixed) serve both.
+__host__ __device__ __forceinline__ uint64_t span_key_pos(uint64_t t) {
+  const uint64_t q = (t >> 2) & 31u;
+  return (((t >> 12) * 4 + (q >> 3)) << 11) | ((q & 7u) << 7) | (((t >> 7) & 31u) << 2) | (t & 3u);
+}
+// inverse for a high-word position u (u & 2047 < 1024)
+__host__ __device__ __forceinline__ uint64_t span_key_slot(uint64_t u) {
+  const uint64_t blk = u >> 11, w = u & 1023u;
+  const uint64_t q = (blk & 3u) * 8 + (w >> 7);
+  return ((blk >> 2) << 12) | (((w >> 2) & 31u) << 7) | (q << 2) | (w & 3u);
+}
+
 __global__ void __launch_bounds__(256) k_span_prefix(uint32_t n, uint32_t lgb, uint32_t ntiles,
                                                      uint4* __restrict__ table) {
-  const uint64_t total = uint64_t(ntiles) * 1024u;
+  // thread per 4 consecutive high-word positions (one uint4 of highs, one of lows)
+  const uint64_t total = uint64_t(ntiles) * 1024u;  // uint4 of high words
   for (uint64_t u = blockIdx.x * 256ull + threadIdx.x; u < total; u += uint64_t(gridDim.x) * 256u) {
-    const uint32_t tile = uint32_t(u >> 10), w = uint32_t(u & 1023u);
-    const uint32_t q = w >> 5, lane = w & 31u;
-    const uint32_t e0 = tile * kWTile + lane * kSpan + q * 4;
+    const uint64_t pos = ((u >> 8) << 11) | ((u & 255u) << 2);  // first high word of the uint4
+    const uint64_t t0 = span_key_slot(pos);
     uint32_t hi[4], lo[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint32_t i = e0 + k;
-      const uint64_t z = i < n ? mix64h(uint64_t(i >> lgb) ^ mix64h(uint64_t(i))) : 0ull;
+      const uint64_t i = t0 + k;
+      const uint64_t z = i < n ? mix64h(uint64_t(i >> lgb) ^ mix64h(i)) : 0ull;
       hi[k] = uint32_t(z >> 32);
       lo[k] = uint32_t(z);
     }
-    table[uint64_t(tile) * 2048 + w] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    table[uint64_t(tile) * 2048 + 1024 + w] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    table[pos >> 2] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    table[(pos >> 2) + 256] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
   }
 }
 
@@ -661,6 +674,102 @@ DspanFn pick_dspan(int bits, uint32_t lgb) {
     case 3: return pick_dspan_lgb<3>(lgb);
     case 4: return pick_dspan_lgb<4>(lgb);
     default: return nullptr;
+  }
+}
+
+// K3 span decode of one tile of a piece (gcx_decode_pieces): as k_dspan with
+// the bucket size a runtime property of the piece (one table entry per chunk,
+// recomputed when the chunk starts a new bucket) and piece-relative offsets.
+template <uint32_t BITS>
+__device__ __forceinline__ void dspan_piece_tile(const gcx_piece& p, uint32_t start, uint32_t count,
+                                                 const uint8_t* __restrict__ msg,
+                                                 float* __restrict__ dst, float div, float recip,
+                                                 bool pow2, uint32_t* words, uint32_t lane) {
+  constexpr uint32_t W = BITS + 1, S = (1u << BITS) - 1, F = 2u << BITS;
+  constexpr uint32_t TW = 128u * W;
+  const uint32_t f = lane & (F - 1u), level = f & S, sign = f >> BITS;
+  const double dl = double(level);
+  const double sd = double(S), ys = __drcp_rn(sd);
+  const uint32_t qbit = 4 * W * lane, qw = qbit >> 5, qsh = qbit & 31u;
+  const bool two = qsh + 4 * W > 32;
+  const uint32_t lgb = 31 - __clz(p.bucket), bshift = lgb - 7;
+  const bool full = count == kWTile;
+  const uint32_t* src =
+      reinterpret_cast<const uint32_t*>(msg + p.packed) + uint64_t(start >> 5) * W;
+  const uint32_t nbk = uint32_t((p.len + p.bucket - 1) >> lgb);
+  const uint32_t b0 = start >> lgb;
+  const uint32_t nreg = lane < (kWTile >> lgb) && b0 + lane < nbk
+                            ? __ldg(reinterpret_cast<const uint32_t*>(msg + p.norms) + b0 + lane)
+                            : 0u;
+  if (full && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+    uint4 st[W];
+#pragma unroll
+    for (uint32_t k = 0; k < W; ++k) st[k] = __ldcs(reinterpret_cast<const uint4*>(src) + k * 32 + lane);
+#pragma unroll
+    for (uint32_t k = 0; k < W; ++k) reinterpret_cast<uint4*>(words)[k * 32 + lane] = st[k];
+  } else {
+    const uint32_t nw = (count * W + 31) / 32;
+    for (uint32_t k = lane; k < TW; k += 32) words[k] = k < nw ? src[k] : 0u;
+  }
+  __syncwarp();
+  float* out = dst + p.src + start + 4 * lane;
+  const bool vec = full && (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+  float entry = 0.0f;
+#pragma unroll 4
+  for (uint32_t c = 0; c < 32; ++c) {
+    if (c * 128 >= count) break;
+    if ((c & ((1u << bshift) - 1u)) == 0) {  // first chunk of a bucket: its table entry
+      const uint32_t nu = __shfl_sync(0xffffffffu, nreg, c >> bshift);
+      const double nl = __dmul_rn(double(__uint_as_float(nu)), dl);  // exact
+      const double q0 = __dmul_rn(nl, ys);
+      const double q = __fma_rn(__fma_rn(-sd, q0, nl), ys, q0);  // RN(nl / s), see dequant_field
+      const float m = apply_divisor(__double2float_rn(q), div, recip, pow2);
+      entry = level == 0 ? 0.0f : (sign ? -m : m);
+    }
+    const uint32_t* cw = words + c * 4 * W + qw;
+    const uint32_t win = two ? __funnelshift_r(cw[0], cw[1], qsh) : (cw[0] >> qsh);
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, entry, (win >> (k * W)) & (F - 1u));
+    float* o = out + c * 128;
+    if (vec) {
+      __stcs(reinterpret_cast<float4*>(o), make_float4(v[0], v[1], v[2], v[3]));
+    } else {
+      const uint32_t e = c * 128 + 4 * lane;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (e + k < count) __stcs(o + k, v[k]);
+    }
+  }
+  __syncwarp();  // words[] is restaged by the next tile
+}
+
+__global__ void __launch_bounds__(32 * kDWarps) k_dspan_pieces(gcx_plan::PlanView pv,
+                                                               const uint8_t* __restrict__ msg,
+                                                               float* __restrict__ dst, float div,
+                                                               float recip, bool pow2) {
+  __shared__ __align__(16) uint32_t words_all[kDWarps][128 * 5];
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t* words = words_all[warp];
+  const uint32_t nw = gridDim.x * kDWarps;
+  for (uint32_t t = blockIdx.x * kDWarps + warp; t < pv.ntiles; t += nw) {
+    gcx_plan::TileCtx c;
+    gcx_plan::locate_warp(pv, t, c);
+    const gcx_piece& p = c.p;
+    switch (p.bits) {
+      case 0: {  // raw piece: f32 payload at p.norms, divided (finalize's average)
+        const float* in = reinterpret_cast<const float*>(msg + p.norms) + c.start;
+        float* out = dst + p.src + c.start;
+        for (uint32_t e = lane; e < c.count; e += 32)
+          __stcs(out + e, apply_divisor(__ldcs(in + e), div, recip, pow2));
+        break;
+      }
+      case 1: dspan_piece_tile<1>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
+      case 2: dspan_piece_tile<2>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
+      case 3: dspan_piece_tile<3>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
+      case 4: dspan_piece_tile<4>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
+      default: break;
+    }
   }
 }
 
@@ -821,5 +930,28 @@ cudaError_t gcx_span_dequantize(const float* norms, const uint8_t* packed, uint6
   if (grid > uint32_t(sms * o)) grid = uint32_t(sms * o);
   if (grid == 0) grid = 1;
   fn<<<grid, 32 * kDWarps, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+bool gcx_span_decode_piece_ok(int bits, uint64_t bucket) {
+  return bits == 0 || gcx_span_decode_supported(bits, bucket);
+}
+
+cudaError_t gcx_span_decode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix,
+                                   uint32_t npieces, uint32_t ntiles, const uint8_t* msg,
+                                   float* dst, float divisor, int sms, cudaStream_t st) {
+  static thread_local int occ = 0;
+  if (occ == 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dspan_pieces, 32 * kDWarps, 0);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+  }
+  gcx_plan::PlanView pv{pieces, tile_prefix, npieces, ntiles, {}};
+  int e2 = 0;
+  const bool pow2 = std::frexp(divisor, &e2) == 0.5f;
+  uint32_t grid = (ntiles + kDWarps - 1) / kDWarps;
+  if (grid > uint32_t(sms * occ)) grid = uint32_t(sms * occ);
+  if (grid == 0) grid = 1;
+  k_dspan_pieces<<<grid, 32 * kDWarps, 0, st>>>(pv, msg, dst, divisor, 1.0f / divisor, pow2);
   return cudaGetLastError();
 }

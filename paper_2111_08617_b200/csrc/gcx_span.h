@@ -5,6 +5,8 @@
 
 #include <cstdint>
 
+#include "gcx.h"
+
 // buckets the span kernel handles (32, 64, 128)
 bool gcx_span_supported(uint64_t bucket);
 // prefix-table slots (8 bytes each) of an n-element vector in span layout
@@ -20,3 +22,9 @@ bool gcx_span_decode_supported(int bits, uint64_t bucket);
 cudaError_t gcx_span_dequantize(const float* norms, const uint8_t* packed, uint64_t n, int bits,
                                 uint64_t bucket, float* out, float divisor, int sms,
                                 cudaStream_t st);
+// K3 span decode over a piece table whose pieces are all raw or
+// span-decodable (gcx_plan_tiles sets GCX_F_SPAN_DEC)
+bool gcx_span_decode_piece_ok(int bits, uint64_t bucket);
+cudaError_t gcx_span_decode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix,
+                                   uint32_t npieces, uint32_t ntiles, const uint8_t* msg,
+                                   float* dst, float divisor, int sms, cudaStream_t st);

@@ -43,7 +43,7 @@ def test_capi_host_helpers(oracle):
     assert _capi.lib().gcx_uniform01(42, 1, 130) == 0.26891814055097596
     # tile planning: one tile per 4096 elements for bucket 128; flags
     nt, prefix, flags = _capi.plan_tiles([_capi.Piece(0, 10000, 0, 0, 0, 128, 4)])
-    assert nt == 3 and prefix == [0, 3] and flags == 0
+    assert nt == 3 and prefix == [0, 3] and flags == 128  # GCX_F_SPAN_DEC
     nt, _, flags = _capi.plan_tiles([_capi.Piece(0, 10000, 0, 0, 0, 1000, 4)])
     # 4000-element tiles x 5 bits = 625 whole words: no zeroing; bucket 1000 takes
     # the generic K1b and the norm pre-pass
