@@ -50,6 +50,11 @@ extern "C" {
 #define GCX_F_KEY_PREFIX 64u   /* the key table holds seed-independent prefixes (gcx_make_prefix) */
 #define GCX_F_SPAN_DEC 128u    /* every piece is raw or bits<=4 with a power-of-two bucket in
                                   [128, 4096]: the shuffle-table span decode serves the table */
+#define GCX_F_SPAN_ENC 256u    /* every quantized piece has the same bits and bucket, bucket in
+                                  {32, 64, 128}: the span K1 serves the table; its key runs use
+                                  the span key layout (gcx_plan_keys) */
+#define GCX_F_SPAN_BITS_SHIFT 16 /* with GCX_F_SPAN_ENC: bits at flags[16..19], */
+#define GCX_F_SPAN_LGB_SHIFT 20  /* log2(bucket) at flags[20..23] */
 
 #define GCX_TILE 4096          /* max elements per CTA tile */
 

@@ -68,4 +68,22 @@ __device__ __forceinline__ void locate_warp(const PlanView& pv, uint32_t t, Tile
   c.count = rem < T ? uint32_t(rem) : T;
 }
 
+// Span key layout (prefix and key tables of the span K1 kernels): slot t of
+// a run (runs start on multiples of 4096 slots) = element t of a piece; with
+// tile T = t >> 12, row r = (t >> 7) & 31, quad q = (t >> 2) & 31, k = t & 3,
+// its high word sits in block b = 4T + q/8 (2048 words: 1024 high words, then
+// the 1024 low words) at (q % 8) * 128 + r * 4 + k.  Blocks of 1024 slots with
+// high words first are also the lane-group layout's (key_pos), so slot-wise
+// passes (gcx_make_keys_prefixed) serve both.
+__host__ __device__ __forceinline__ uint64_t span_key_pos(uint64_t t) {
+  const uint64_t q = (t >> 2) & 31u;
+  return (((t >> 12) * 4 + (q >> 3)) << 11) | ((q & 7u) << 7) | (((t >> 7) & 31u) << 2) | (t & 3u);
+}
+// inverse for a high-word position u (u & 2047 < 1024)
+__host__ __device__ __forceinline__ uint64_t span_key_slot(uint64_t u) {
+  const uint64_t blk = u >> 11, w = u & 1023u;
+  const uint64_t q = (blk & 3u) * 8 + (w >> 7);
+  return ((blk >> 2) << 12) | (((w >> 2) & 31u) << 7) | (q << 2) | (w & 3u);
+}
+
 }  // namespace gcx_plan

@@ -53,6 +53,8 @@
 namespace gcx_span {
 
 using namespace gcx_dev;
+using gcx_plan::span_key_pos;
+using gcx_plan::span_key_slot;
 
 constexpr uint32_t kSpan = 128;          // elements per lane row
 constexpr uint32_t kWTile = 32 * kSpan;  // elements per warp tile
@@ -502,22 +504,270 @@ __global__ void __launch_bounds__(32 * kWarps, 1)
   if (A.p_al16 && lane == 0) bulk_wait0();  // bulk stores complete before exit
 }
 
-// Span key layout (prefix and key tables of the span K1 kernels): slot t of
-// a run (runs start on multiples of 4096 slots) = element t of a piece; with
-// tile T = t >> 12, row r = (t >> 7) & 31, quad q = (t >> 2) & 31, k = t & 3,
-// its high word sits in block b = 4T + q/8 (2048 words: 1024 high words, then
-// the 1024 low words) at (q % 8) * 128 + r * 4 + k.  Blocks of 1024 slots with
-// high words first are also the lane-group layout's (key_pos), so slot-wise
-// passes (gcx_make_keys_prefixed) serve both.
-__host__ __device__ __forceinline__ uint64_t span_key_pos(uint64_t t) {
-  const uint64_t q = (t >> 2) & 31u;
-  return (((t >> 12) * 4 + (q >> 3)) << 11) | ((q & 7u) << 7) | (((t >> 7) & 31u) << 2) | (t & 3u);
+// ---------------------------------------------------------------------------
+// K1 span over a piece table (gcx_encode_pieces: SRA stage 1, the owner's
+// re-encode, the engine's buffers) whose quantized pieces all share one
+// (bits, bucket in {32, 64, 128}) — GCX_F_SPAN_ENC from gcx_plan_tiles.  Same
+// passes and key ring as k_span; per tile the piece is located in the tile
+// prefix (pieces are piece-local: bucket and key indices restart at every
+// piece, codec.cpp:60 via collectives.cpp:143-163).  Tiles are staged by
+// zero-filling cp.async copies (piece offsets are arbitrary, so no tensor map
+// describes them), completion counted on the slot's mbarrier
+// (cp.async.mbarrier.arrive.noinc, one arrival per lane).  Raw pieces are
+// copied into the message by the warp.  Keys: inline, or span-layout
+// prefixes at run offset p.keys (gcx_plan_keys / gcx_make_key_prefix).
+// ---------------------------------------------------------------------------
+struct SpanPiecesArgs {
+  gcx_plan::PlanView pv;
+  uint32_t flags;
+  uint64_t seed;
+  const float* src;
+  uint8_t* msg;
+  const uint32_t* keys;  // span-layout prefix words or nullptr (inline)
+  unsigned long long* bad;
+};
+
+__device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(src_bytes)
+               : "memory");
 }
-// inverse for a high-word position u (u & 2047 < 1024)
-__host__ __device__ __forceinline__ uint64_t span_key_slot(uint64_t u) {
-  const uint64_t blk = u >> 11, w = u & 1023u;
-  const uint64_t q = (blk & 3u) * 8 + (w >> 7);
-  return ((blk >> 2) << 12) | (((w >> 2) & 31u) << 7) | (q << 2) | (w & 3u);
+__device__ __forceinline__ void cp_async4z(void* smem, const void* gmem, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <uint32_t BITS, int LGB, bool PREFIX>
+__global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A) {
+  constexpr uint32_t W = BITS + 1;
+  constexpr uint32_t BL = 1u << LGB;
+  constexpr uint32_t NB = kSpan / BL;
+  constexpr uint32_t GPB = BL / 32;
+  extern __shared__ __align__(1024) unsigned char span_smem[];
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  unsigned char* base = span_smem + warp * warp_smem_bytes(W);
+  float* slots = reinterpret_cast<float*>(base);
+  uint32_t* outw = reinterpret_cast<uint32_t*>(base + kSlots * kSlotFloats * 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + kSlots * kSlotFloats * 4 + out_words(W) * 4);
+  const uint32_t gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+  const uint32_t ntiles = A.pv.ntiles;
+  const HashK shk = make_hashk();
+  const bool piece_seeds = (A.flags & GCX_F_PIECE_SEEDS) != 0;
+
+  if (lane == 0) {
+    for (uint32_t s = 0; s < kSlots; ++s) mbar_init(bars + s, 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  // Tile contexts: each tile is located once (locate_warp searches the tile
+  // prefix) and kept in the warp's shared slot `memo` until the next tile is
+  // located: the quarters of a tile are issued back to back and the main
+  // loop's look-ahead asks for the tile the last issue located.
+  __shared__ gcx_plan::TileCtx memo_all[kWarps];
+  __shared__ uint32_t memo_t[kWarps];
+  gcx_plan::TileCtx& memo = memo_all[warp];
+  if (lane == 0) memo_t[warp] = ~0u;
+  __syncwarp();
+  auto ctx_of = [&](uint32_t t, gcx_plan::TileCtx& c) {
+    if (memo_t[warp] == t) {
+      c = memo;
+      return;
+    }
+    gcx_plan::locate_warp(A.pv, t, c);
+    __syncwarp();
+    if (lane == 0) {
+      memo = c;
+      memo_t[warp] = t;
+    }
+    __syncwarp();
+  };
+  // quarter Q = quarter Q % 4 of this warp's (Q / 4)-th tile, slot Q % 5
+  auto issue = [&](uint32_t Q) {
+    const uint32_t t = gw + (Q >> 2) * nw, g = Q & 3u;
+    if (t >= ntiles) return;
+    gcx_plan::TileCtx c;
+    ctx_of(t, c);
+    uint64_t* bar = bars + Q % kSlots;
+    if (c.p.bits > 0) {
+      float* dst = slots + (Q % kSlots) * kSlotFloats;
+      const float* x = A.src + c.p.src + c.start + g * 32;
+      if ((reinterpret_cast<uintptr_t>(A.src + c.p.src) & 15u) == 0) {
+#pragma unroll
+        for (uint32_t m = 0; m < 8; ++m) {  // lanes 8r'..8r'+7: one row's 128 bytes
+          const uint32_t r = 4 * m + (lane >> 3), ch = lane & 7u;
+          const uint32_t e = r * kSpan + g * 32 + ch * 4;
+          const uint32_t nb = e >= c.count ? 0u : min(4u, c.count - e) * 4u;
+          cp_async16z(dst + r * 32 + ((ch ^ (r & 7u)) << 2), nb ? x + r * kSpan + ch * 4 : A.src, nb);
+        }
+      } else {
+        for (uint32_t r = 0; r < 32; ++r) {
+          const uint32_t e = r * kSpan + g * 32 + lane;
+          cp_async4z(dst + swz(r, lane), e < c.count ? x + r * kSpan + lane : A.src, e < c.count ? 4u : 0u);
+        }
+      }
+    }
+    cp_async_mbar_arrive(bar);  // raw tiles: the phase completes at once
+  };
+  auto wait_q = [&](uint32_t Q) { mbar_wait(bars + Q % kSlots, (Q / kSlots) & 1u); };
+  auto key_group = [&](const gcx_plan::TileCtx& c, uint32_t g) -> const uint4* {
+    return reinterpret_cast<const uint4*>(A.keys) + ((c.p.keys + c.start) >> 12) * 2048 + g * 512 + lane;
+  };
+
+  uint4 kh[8], kl[8];
+  gcx_plan::TileCtx cur;
+  if (gw < ntiles) {
+    ctx_of(gw, cur);
+    if (PREFIX && cur.p.bits > 0) {
+      const uint4* k0 = key_group(cur, 0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        kh[q] = __ldg(k0 + q * 32);
+        kl[q] = __ldg(k0 + 256 + q * 32);
+      }
+    }
+  }
+  for (uint32_t Q = 0; Q < kSlots; ++Q) issue(Q);
+
+  uint32_t j = 0;
+  for (uint32_t t = gw; t < ntiles; t += nw, ++j) {
+    const bool more = t + nw < ntiles;
+    gcx_plan::TileCtx nxt;
+    if (more) ctx_of(t + nw, nxt);
+    const gcx_piece& p = cur.p;
+    if (p.bits == 0) {  // raw piece: its f32 values are the payload (collectives.cpp:153-158)
+      const float* xs = A.src + p.src + cur.start;
+      float* d = reinterpret_cast<float*>(A.msg + p.norms) + cur.start;
+      for (uint32_t e = lane; e < cur.count; e += 32) d[e] = __ldcs(xs + e);
+      if (PREFIX && more && nxt.p.bits > 0) {  // the key ring's next group
+        const uint4* kn = key_group(nxt, 0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          kh[q] = __ldg(kn + q * 32);
+          kl[q] = __ldg(kn + 256 + q * 32);
+        }
+      }
+#pragma unroll 1
+      for (uint32_t g = 0; g < 4; ++g) {
+        __syncwarp();
+        issue(4 * j + g + kSlots);
+      }
+      cur = nxt;
+      continue;
+    }
+    const uint64_t seed = piece_seeds ? p.seed : A.seed;
+    const uint32_t s_lo = uint32_t(seed), s_hi = uint32_t(seed >> 32);
+    const bool full = cur.count == kWTile;
+    const uint32_t i_lane = cur.start + lane * kSpan;  // piece-local first element of the row
+    uint32_t* norms = reinterpret_cast<uint32_t*>(A.msg + p.norms);
+    const unsigned long long pkey = uint64_t(cur.pidx) << 40;
+    RowView rv;
+#pragma unroll
+    for (uint32_t g = 0; g < 4; ++g) rv.slot[g] = slots + ((4 * j + g) % kSlots) * kSlotFloats;
+    rv.r = lane;
+
+    // ---- pass 1 ----
+    uint32_t nu[NB];
+    bool careful[NB];
+    {
+      double sq = 0.0;
+#pragma unroll
+      for (uint32_t g = 0; g < 4; ++g) {
+        wait_q(4 * j + g);
+        const float* row = rv.slot[g] + lane * 32u;
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q) {
+          const float4 v = *reinterpret_cast<const float4*>(row + ((q ^ (lane & 7u)) << 2));
+          double d = double(v.x);
+          sq = __fma_rn(d, d, sq);
+          d = double(v.y);
+          sq = __fma_rn(d, d, sq);
+          d = double(v.z);
+          sq = __fma_rn(d, d, sq);
+          d = double(v.w);
+          sq = __fma_rn(d, d, sq);
+        }
+        if ((g * 32 + 32) % BL == 0) {
+          const uint32_t r = (g * 32) / BL;
+          const bool c = (uint32_t(__double2hiint(sq)) & 0x7FF00000u) == 0x7FF00000u;
+          uint32_t v;
+          if (c) {
+            v = span_norm_exact(rv, r * BL, BL, 0u, nullptr);
+            if (A.bad != nullptr) {  // first non-finite: (piece << 40) | piece-local index
+              for (uint32_t e = 0; e < BL; ++e)
+                if ((__float_as_uint(rv.at(r * BL + e)) & 0x7FFFFFFFu) >= 0x7F800000u) {
+                  atomicMin(A.bad, pkey | (i_lane + r * BL + e));
+                  break;
+                }
+            }
+          } else {
+            v = __float_as_uint(__double2float_rn(__dsqrt_rn(sq)));
+          }
+#pragma unroll
+          for (uint32_t rr = 0; rr < NB; ++rr)
+            if (rr == r) {
+              nu[rr] = v;
+              careful[rr] = c;
+            }
+          if (i_lane + r * BL < p.len) norms[(i_lane >> LGB) + r] = v;
+          sq = 0.0;
+        }
+      }
+    }
+
+    // ---- pass 2 ----
+    if (lane == 0) bulk_wait_read0();
+    __syncwarp();
+    const uint4* kp = PREFIX ? key_group(cur, 0) : nullptr;
+    const uint4* kp_next = PREFIX && more && nxt.p.bits > 0 ? key_group(nxt, 0) : nullptr;
+#pragma unroll 1
+    for (uint32_t g = 0; g < 4; ++g) {
+      const uint32_t r = g / GPB;
+      uint32_t nug = nu[0];
+      bool car = careful[0];
+#pragma unroll
+      for (uint32_t rr = 1; rr < NB; ++rr)
+        if (r == rr) {
+          nug = nu[rr];
+          car = careful[rr];
+        }
+      const uint32_t i0 = i_lane + g * 32;
+      const uint4* kn = g < 3 ? kp + (g + 1) * 512 : kp_next;
+      const float* slot = slots + ((4 * j + g) % kSlots) * kSlotFloats;
+      uint32_t* wout = outw + (lane * 4 + g) * W;
+      uint32_t w[W];
+      const bool ok = span_group_fast<BITS, LGB, PREFIX>(slot, lane, i0, nug, s_lo, s_hi, shk, w, kh,
+                                                         kl, kn) &&
+                      nug != 0u && !car;
+      if (ok) {
+#pragma unroll
+        for (int m = 0; m < int(W); ++m) wout[m] = w[m];
+      } else {
+        span_group_exact<BITS, LGB, PREFIX>(
+            rv, g, i0, nug, seed,
+            PREFIX ? A.keys + ((p.keys + cur.start) >> 12) * 8192u : nullptr, lane, wout);
+      }
+      __syncwarp();
+      issue(4 * j + g + kSlots);
+    }
+    __syncwarp();
+    uint32_t* dstw = reinterpret_cast<uint32_t*>(A.msg + p.packed) + uint64_t(cur.start >> 5) * W;
+    if (full && (reinterpret_cast<uintptr_t>(dstw) & 15u) == 0) {
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) bulk_s2g(dstw, outw, out_words(W) * 4);
+    } else {
+      const uint32_t nwords = (cur.count * W + 31) / 32;
+      for (uint32_t e = lane; e < nwords; e += 32) dstw[e] = outw[e];
+    }
+    __syncwarp();
+    cur = nxt;
+  }
+  if (lane == 0) bulk_wait0();
 }
 
 __global__ void __launch_bounds__(256) k_span_prefix(uint32_t n, uint32_t lgb, uint32_t ntiles,
@@ -714,31 +964,40 @@ __device__ __forceinline__ void dspan_piece_tile(const gcx_piece& p, uint32_t st
   __syncwarp();
   float* out = dst + p.src + start + 4 * lane;
   const bool vec = full && (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
-  float entry = 0.0f;
-#pragma unroll 4
-  for (uint32_t c = 0; c < 32; ++c) {
-    if (c * 128 >= count) break;
-    if ((c & ((1u << bshift) - 1u)) == 0) {  // first chunk of a bucket: its table entry
-      const uint32_t nu = __shfl_sync(0xffffffffu, nreg, c >> bshift);
+  // batches of 8 chunks: 8 independent FP64 chains for the batch's table
+  // entries (one per chunk; chunks of one bucket compute the same entry),
+  // then 8 chunks decoded by shuffles
+#pragma unroll 1
+  for (uint32_t bb = 0; bb < 4; ++bb) {
+    if (bb * 1024 >= count) break;
+    float entry[8];
+#pragma unroll
+    for (uint32_t cc = 0; cc < 8; ++cc) {
+      const uint32_t nu = __shfl_sync(0xffffffffu, nreg, (bb * 8 + cc) >> bshift);
       const double nl = __dmul_rn(double(__uint_as_float(nu)), dl);  // exact
       const double q0 = __dmul_rn(nl, ys);
       const double q = __fma_rn(__fma_rn(-sd, q0, nl), ys, q0);  // RN(nl / s), see dequant_field
       const float m = apply_divisor(__double2float_rn(q), div, recip, pow2);
-      entry = level == 0 ? 0.0f : (sign ? -m : m);
+      entry[cc] = level == 0 ? 0.0f : (sign ? -m : m);
     }
-    const uint32_t* cw = words + c * 4 * W + qw;
-    const uint32_t win = two ? __funnelshift_r(cw[0], cw[1], qsh) : (cw[0] >> qsh);
-    float v[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, entry, (win >> (k * W)) & (F - 1u));
-    float* o = out + c * 128;
-    if (vec) {
-      __stcs(reinterpret_cast<float4*>(o), make_float4(v[0], v[1], v[2], v[3]));
-    } else {
-      const uint32_t e = c * 128 + 4 * lane;
+    for (uint32_t cc = 0; cc < 8; ++cc) {
+      const uint32_t c = bb * 8 + cc;
+      if (c * 128 >= count) break;
+      const uint32_t* cw = words + c * 4 * W + qw;
+      const uint32_t win = two ? __funnelshift_r(cw[0], cw[1], qsh) : (cw[0] >> qsh);
+      float v[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (e + k < count) __stcs(o + k, v[k]);
+      for (int k = 0; k < 4; ++k) v[k] = __shfl_sync(0xffffffffu, entry[cc], (win >> (k * W)) & (F - 1u));
+      float* o = out + c * 128;
+      if (vec) {
+        __stcs(reinterpret_cast<float4*>(o), make_float4(v[0], v[1], v[2], v[3]));
+      } else {
+        const uint32_t e = c * 128 + 4 * lane;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (e + k < count) __stcs(o + k, v[k]);
+      }
     }
   }
   __syncwarp();  // words[] is restaged by the next tile
@@ -953,5 +1212,64 @@ cudaError_t gcx_span_decode_pieces(const gcx_piece* pieces, const uint32_t* tile
   if (grid > uint32_t(sms * occ)) grid = uint32_t(sms * occ);
   if (grid == 0) grid = 1;
   k_dspan_pieces<<<grid, 32 * kDWarps, 0, st>>>(pv, msg, dst, divisor, 1.0f / divisor, pow2);
+  return cudaGetLastError();
+}
+
+using SpanPiecesFn = void (*)(SpanPiecesArgs);
+
+template <uint32_t BITS>
+SpanPiecesFn pick_pieces_lgb(int lgb, bool prefix) {
+  switch (lgb) {
+    case 5: return prefix ? k_span_pieces<BITS, 5, true> : k_span_pieces<BITS, 5, false>;
+    case 6: return prefix ? k_span_pieces<BITS, 6, true> : k_span_pieces<BITS, 6, false>;
+    case 7: return prefix ? k_span_pieces<BITS, 7, true> : k_span_pieces<BITS, 7, false>;
+    default: return nullptr;
+  }
+}
+
+static SpanPiecesFn pick_pieces(int bits, int lgb, bool prefix) {
+  switch (bits) {
+    case 1: return pick_pieces_lgb<1>(lgb, prefix);
+    case 2: return pick_pieces_lgb<2>(lgb, prefix);
+    case 3: return pick_pieces_lgb<3>(lgb, prefix);
+    case 4: return pick_pieces_lgb<4>(lgb, prefix);
+    case 5: return pick_pieces_lgb<5>(lgb, prefix);
+    case 6: return pick_pieces_lgb<6>(lgb, prefix);
+    case 7: return pick_pieces_lgb<7>(lgb, prefix);
+    case 8: return pick_pieces_lgb<8>(lgb, prefix);
+    default: return nullptr;
+  }
+}
+
+cudaError_t gcx_span_encode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix,
+                                   uint32_t npieces, uint32_t ntiles, uint32_t flags, uint64_t seed,
+                                   const float* src, uint8_t* msg, const unsigned long long* prefix,
+                                   unsigned long long* bad, int sms, cudaStream_t st) {
+  const int bits = int((flags >> GCX_F_SPAN_BITS_SHIFT) & 15u);
+  const int lgb = int((flags >> GCX_F_SPAN_LGB_SHIFT) & 15u);
+  SpanPiecesFn fn = pick_pieces(bits, lgb, prefix != nullptr);
+  if (fn == nullptr) return cudaErrorInvalidValue;
+  const size_t smem = size_t(kWarps) * warp_smem_bytes(uint32_t(bits) + 1);
+  static thread_local int occ[9][8][2] = {};
+  int& o = occ[bits][lgb][prefix != nullptr];
+  if (o == 0) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 32 * kWarps, smem);
+    if (e != cudaSuccess) return e;
+    if (o < 1) o = 1;
+  }
+  SpanPiecesArgs a;
+  a.pv = gcx_plan::PlanView{pieces, tile_prefix, npieces, ntiles, {}};
+  a.flags = flags;
+  a.seed = seed;
+  a.src = src;
+  a.msg = msg;
+  a.keys = reinterpret_cast<const uint32_t*>(prefix);
+  a.bad = bad;
+  uint32_t grid = (ntiles + kWarps - 1) / kWarps;
+  if (grid > uint32_t(sms * o)) grid = uint32_t(sms * o);
+  if (grid == 0) grid = 1;
+  fn<<<grid, 32 * kWarps, smem, st>>>(a);
   return cudaGetLastError();
 }

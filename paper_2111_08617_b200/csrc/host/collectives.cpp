@@ -341,6 +341,13 @@ void encode(const TableBlob& blob, const Table& t, std::uint64_t seed, const flo
             std::uint8_t* msg, unsigned long long* keys, unsigned long long* bad,
             cudaStream_t st, const unsigned long long* key_prefix = nullptr) {
   const bool use_keys = keys != nullptr && t.key_len > 0;
+  if (t.flags & GCX_F_SPAN_ENC) {  // span K1: one launch, from the prefixes or hashing inline
+    const bool pre = use_keys && key_prefix != nullptr;
+    gcx_check(gcx_encode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
+                                t.ntiles, t.flags | (pre ? GCX_F_KEY_PREFIX : 0u), seed, src, msg,
+                                pre ? key_prefix : nullptr, bad, st));
+    return;
+  }
   if (use_keys && key_prefix != nullptr && onestep(t)) {
     gcx_check(gcx_encode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
                                 t.ntiles, t.flags | GCX_F_KEY_PREFIX, seed, src, msg, key_prefix,

@@ -43,7 +43,8 @@ def test_capi_host_helpers(oracle):
     assert _capi.lib().gcx_uniform01(42, 1, 130) == 0.26891814055097596
     # tile planning: one tile per 4096 elements for bucket 128; flags
     nt, prefix, flags = _capi.plan_tiles([_capi.Piece(0, 10000, 0, 0, 0, 128, 4)])
-    assert nt == 3 and prefix == [0, 3] and flags == 128  # GCX_F_SPAN_DEC
+    assert nt == 3 and prefix == [0, 3]
+    assert flags == 128 | 256 | (4 << 16) | (7 << 20)  # GCX_F_SPAN_DEC | GCX_F_SPAN_ENC, 4 bits, bucket 2^7
     nt, _, flags = _capi.plan_tiles([_capi.Piece(0, 10000, 0, 0, 0, 1000, 4)])
     # 4000-element tiles x 5 bits = 625 whole words: no zeroing; bucket 1000 takes
     # the generic K1b and the norm pre-pass
