@@ -139,6 +139,14 @@ int gcx_encode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint
  * plan_keys sets pieces[k].keys, fills groups[], returns the table length. */
 int64_t gcx_plan_keys(gcx_piece* pieces, uint32_t npieces, gcx_keygroup* groups,
                       uint32_t group_cap, uint32_t* ngroups);
+/* Same, choosing the key-table layout: GCX_KEYS_AUTO = the span layout when
+ * the table qualifies for the span K1 (GCX_F_SPAN_ENC), GCX_KEYS_LANE_GROUP =
+ * always the lane-group layout (the caller then clears GCX_F_SPAN_ENC from the
+ * table's flags, so the lane-group K1 kernels read it). */
+#define GCX_KEYS_AUTO 0
+#define GCX_KEYS_LANE_GROUP 1
+int64_t gcx_plan_keys_layout(gcx_piece* pieces, uint32_t npieces, gcx_keygroup* groups,
+                             uint32_t group_cap, uint32_t* ngroups, int layout);
 int gcx_make_keys(const gcx_keygroup* groups, uint32_t ngroups, uint64_t total, uint64_t seed,
                   unsigned long long* keys, void* stream);
 /* The same table in two steps for layouts that are reused every step (an

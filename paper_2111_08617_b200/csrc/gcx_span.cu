@@ -200,7 +200,12 @@ __device__ __forceinline__ void put_field(uint32_t (&w)[W], uint32_t j, uint32_t
 // exact per-element path for group g of a lane's row (any inputs); writes the
 // group's W words to w.  Keys: prefix table words of the tile (hi at
 // ph[quad*128 + lane*4 + k], lo 4096 words later) or inline hashing.
-template <uint32_t BITS, int LGB, bool PREFIX>
+// key sources of the span K1 kernels
+constexpr int kKmInline = 0;  // three SplitMix64 finalizers per element
+constexpr int kKmTable = 1;   // full keys from a per-step table (gcx_make_keys*), span layout
+constexpr int kKmPrefix = 2;  // seed-independent prefixes T(i), span layout: one finalizer
+
+template <uint32_t BITS, int LGB, int KM>
 __device__ __noinline__ void span_group_exact(RowView rv, uint32_t g, uint32_t i0, uint32_t nu,
                                               uint64_t seed, const uint32_t* ph, uint32_t lane,
                                               uint32_t* w) {
@@ -213,12 +218,17 @@ __device__ __noinline__ void span_group_exact(RowView rv, uint32_t g, uint32_t i
     const double y = __drcp_rn(nd);
     for (uint32_t j = 0; j < 32; ++j) {
       uint32_t hl, hh;
-      if (PREFIX) {  // ph: the tile's first key word (span_key_pos)
+      if (KM != kKmInline) {  // ph: the tile's first key word (span_key_pos)
         const uint32_t pos = g * 2048u + (j >> 2) * 128u + lane * 4u + (j & 3u);
-        const uint64_t z = (uint64_t(ph[pos]) << 32 | ph[pos + 1024]) ^ seed;
-        const uint64_t h = mix64h(z);
-        hl = uint32_t(h);
-        hh = uint32_t(h >> 32);
+        if (KM == kKmTable) {
+          hh = ph[pos];
+          hl = ph[pos + 1024];
+        } else {
+          const uint64_t z = (uint64_t(ph[pos]) << 32 | ph[pos + 1024]) ^ seed;
+          const uint64_t h = mix64h(z);
+          hl = uint32_t(h);
+          hh = uint32_t(h >> 32);
+        }
       } else {
         const uint32_t i = i0 + j;
         draw_key(i, 0u, i >> LGB, 0u, uint32_t(seed), uint32_t(seed >> 32), opq, hl, hh);
@@ -283,7 +293,7 @@ __device__ __forceinline__ float4 lds_v4(const float* p) {
 // keys (kn, or nothing when kn == nullptr) are loaded into the ring, then the
 // elements are quantized — the loads are volatile so they stay ahead of the
 // shared-memory reads and get a whole group of work to land.
-template <uint32_t BITS, int LGB, bool PREFIX>
+template <uint32_t BITS, int LGB, int KM>
 __device__ __forceinline__ bool span_group_fast(const float* slot, uint32_t lane, uint32_t i0,
                                                 uint32_t nu, uint32_t s_lo, uint32_t s_hi,
                                                 const HashK& shk, uint32_t (&w)[BITS + 1],
@@ -293,7 +303,7 @@ __device__ __forceinline__ bool span_group_fast(const float* slot, uint32_t lane
   const float* row = slot + lane * 32u;
   const uint32_t key = lane & 7u;
   uint32_t hh[32];
-  if (PREFIX) {
+  if (KM == kKmPrefix) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       hh[4 * q + 0] = key_hraw_from_prefix(kl[q].x, kh[q].x, s_lo, s_hi, shk);
@@ -301,12 +311,20 @@ __device__ __forceinline__ bool span_group_fast(const float* slot, uint32_t lane
       hh[4 * q + 2] = key_hraw_from_prefix(kl[q].z, kh[q].z, s_lo, s_hi, shk);
       hh[4 * q + 3] = key_hraw_from_prefix(kl[q].w, kh[q].w, s_lo, s_hi, shk);
     }
-    if (kn != nullptr) {
+  } else if (KM == kKmTable) {  // the final key's top word (the compare window covers it)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        kh[q] = ldg_nc_v4(kn + q * 32);
-        kl[q] = ldg_nc_v4(kn + 256 + q * 32);
-      }
+    for (int q = 0; q < 8; ++q) {
+      hh[4 * q + 0] = kh[q].x;
+      hh[4 * q + 1] = kh[q].y;
+      hh[4 * q + 2] = kh[q].z;
+      hh[4 * q + 3] = kh[q].w;
+    }
+  }
+  if (KM != kKmInline && kn != nullptr) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      kh[q] = ldg_nc_v4(kn + q * 32);
+      if (KM == kKmPrefix) kl[q] = ldg_nc_v4(kn + 256 + q * 32);
     }
   }
   const double nd = f32abs_to_f64(nu);
@@ -319,7 +337,7 @@ __device__ __forceinline__ bool span_group_fast(const float* slot, uint32_t lane
     const float4 v = lds_v4(row + ((uint32_t(q) ^ key) << 2));
     const uint32_t u[4] = {__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z),
                            __float_as_uint(v.w)};
-    if (!PREFIX) {
+    if (KM == kKmInline) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) hh[4 * q + k] = key_hraw_inline(i0 + 4 * q + k, b, s_lo, s_hi, shk);
     }
@@ -474,14 +492,14 @@ __global__ void __launch_bounds__(32 * kWarps, 1)
       // into registers the key-ring loads are pending on.
       uint32_t* wout = outw + (lane * 4 + g) * W;
       uint32_t w[W];
-      const bool ok = span_group_fast<BITS, LGB, PREFIX>(slot, lane, i0, nug, s_lo, s_hi, shk, w, kh,
-                                                         kl, kn) &&
+      const bool ok = span_group_fast<BITS, LGB, PREFIX ? kKmPrefix : kKmInline>(
+                          slot, lane, i0, nug, s_lo, s_hi, shk, w, kh, kl, kn) &&
                       nug != 0u && !car;
       if (ok) {
 #pragma unroll
         for (int m = 0; m < int(W); ++m) wout[m] = w[m];
       } else {
-        span_group_exact<BITS, LGB, PREFIX>(rv, g, i0, nug, A.seed,
+        span_group_exact<BITS, LGB, PREFIX ? kKmPrefix : kKmInline>(rv, g, i0, nug, A.seed,
                                             PREFIX ? A.prefix + uint64_t(t) * 8192u : nullptr, lane,
                                             wout);
       }
@@ -541,7 +559,7 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <uint32_t BITS, int LGB, bool PREFIX>
+template <uint32_t BITS, int LGB, int KM>
 __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A) {
   constexpr uint32_t W = BITS + 1;
   constexpr uint32_t BL = 1u << LGB;
@@ -622,12 +640,12 @@ __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A
   gcx_plan::TileCtx cur;
   if (gw < ntiles) {
     ctx_of(gw, cur);
-    if (PREFIX && cur.p.bits > 0) {
+    if (KM != kKmInline && cur.p.bits > 0) {
       const uint4* k0 = key_group(cur, 0);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         kh[q] = __ldg(k0 + q * 32);
-        kl[q] = __ldg(k0 + 256 + q * 32);
+        if (KM == kKmPrefix) kl[q] = __ldg(k0 + 256 + q * 32);
       }
     }
   }
@@ -643,12 +661,12 @@ __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A
       const float* xs = A.src + p.src + cur.start;
       float* d = reinterpret_cast<float*>(A.msg + p.norms) + cur.start;
       for (uint32_t e = lane; e < cur.count; e += 32) d[e] = __ldcs(xs + e);
-      if (PREFIX && more && nxt.p.bits > 0) {  // the key ring's next group
+      if (KM != kKmInline && more && nxt.p.bits > 0) {  // the key ring's next group
         const uint4* kn = key_group(nxt, 0);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           kh[q] = __ldg(kn + q * 32);
-          kl[q] = __ldg(kn + 256 + q * 32);
+          if (KM == kKmPrefix) kl[q] = __ldg(kn + 256 + q * 32);
         }
       }
 #pragma unroll 1
@@ -722,8 +740,8 @@ __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A
     // ---- pass 2 ----
     if (lane == 0) bulk_wait_read0();
     __syncwarp();
-    const uint4* kp = PREFIX ? key_group(cur, 0) : nullptr;
-    const uint4* kp_next = PREFIX && more && nxt.p.bits > 0 ? key_group(nxt, 0) : nullptr;
+    const uint4* kp = KM != kKmInline ? key_group(cur, 0) : nullptr;
+    const uint4* kp_next = KM != kKmInline && more && nxt.p.bits > 0 ? key_group(nxt, 0) : nullptr;
 #pragma unroll 1
     for (uint32_t g = 0; g < 4; ++g) {
       const uint32_t r = g / GPB;
@@ -740,16 +758,16 @@ __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A
       const float* slot = slots + ((4 * j + g) % kSlots) * kSlotFloats;
       uint32_t* wout = outw + (lane * 4 + g) * W;
       uint32_t w[W];
-      const bool ok = span_group_fast<BITS, LGB, PREFIX>(slot, lane, i0, nug, s_lo, s_hi, shk, w, kh,
+      const bool ok = span_group_fast<BITS, LGB, KM>(slot, lane, i0, nug, s_lo, s_hi, shk, w, kh,
                                                          kl, kn) &&
                       nug != 0u && !car;
       if (ok) {
 #pragma unroll
         for (int m = 0; m < int(W); ++m) wout[m] = w[m];
       } else {
-        span_group_exact<BITS, LGB, PREFIX>(
+        span_group_exact<BITS, LGB, KM>(
             rv, g, i0, nug, seed,
-            PREFIX ? A.keys + ((p.keys + cur.start) >> 12) * 8192u : nullptr, lane, wout);
+            KM != kKmInline ? A.keys + ((p.keys + cur.start) >> 12) * 8192u : nullptr, lane, wout);
       }
       __syncwarp();
       issue(4 * j + g + kSlots);
@@ -1217,41 +1235,51 @@ cudaError_t gcx_span_decode_pieces(const gcx_piece* pieces, const uint32_t* tile
 
 using SpanPiecesFn = void (*)(SpanPiecesArgs);
 
+template <uint32_t BITS, int LGB>
+SpanPiecesFn pick_pieces_km(int km) {
+  switch (km) {
+    case kKmTable: return k_span_pieces<BITS, LGB, kKmTable>;
+    case kKmPrefix: return k_span_pieces<BITS, LGB, kKmPrefix>;
+    default: return k_span_pieces<BITS, LGB, kKmInline>;
+  }
+}
+
 template <uint32_t BITS>
-SpanPiecesFn pick_pieces_lgb(int lgb, bool prefix) {
+SpanPiecesFn pick_pieces_lgb(int lgb, int km) {
   switch (lgb) {
-    case 5: return prefix ? k_span_pieces<BITS, 5, true> : k_span_pieces<BITS, 5, false>;
-    case 6: return prefix ? k_span_pieces<BITS, 6, true> : k_span_pieces<BITS, 6, false>;
-    case 7: return prefix ? k_span_pieces<BITS, 7, true> : k_span_pieces<BITS, 7, false>;
+    case 5: return pick_pieces_km<BITS, 5>(km);
+    case 6: return pick_pieces_km<BITS, 6>(km);
+    case 7: return pick_pieces_km<BITS, 7>(km);
     default: return nullptr;
   }
 }
 
-static SpanPiecesFn pick_pieces(int bits, int lgb, bool prefix) {
+static SpanPiecesFn pick_pieces(int bits, int lgb, int km) {
   switch (bits) {
-    case 1: return pick_pieces_lgb<1>(lgb, prefix);
-    case 2: return pick_pieces_lgb<2>(lgb, prefix);
-    case 3: return pick_pieces_lgb<3>(lgb, prefix);
-    case 4: return pick_pieces_lgb<4>(lgb, prefix);
-    case 5: return pick_pieces_lgb<5>(lgb, prefix);
-    case 6: return pick_pieces_lgb<6>(lgb, prefix);
-    case 7: return pick_pieces_lgb<7>(lgb, prefix);
-    case 8: return pick_pieces_lgb<8>(lgb, prefix);
+    case 1: return pick_pieces_lgb<1>(lgb, km);
+    case 2: return pick_pieces_lgb<2>(lgb, km);
+    case 3: return pick_pieces_lgb<3>(lgb, km);
+    case 4: return pick_pieces_lgb<4>(lgb, km);
+    case 5: return pick_pieces_lgb<5>(lgb, km);
+    case 6: return pick_pieces_lgb<6>(lgb, km);
+    case 7: return pick_pieces_lgb<7>(lgb, km);
+    case 8: return pick_pieces_lgb<8>(lgb, km);
     default: return nullptr;
   }
 }
 
 cudaError_t gcx_span_encode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix,
                                    uint32_t npieces, uint32_t ntiles, uint32_t flags, uint64_t seed,
-                                   const float* src, uint8_t* msg, const unsigned long long* prefix,
+                                   const float* src, uint8_t* msg, const unsigned long long* keys,
                                    unsigned long long* bad, int sms, cudaStream_t st) {
   const int bits = int((flags >> GCX_F_SPAN_BITS_SHIFT) & 15u);
   const int lgb = int((flags >> GCX_F_SPAN_LGB_SHIFT) & 15u);
-  SpanPiecesFn fn = pick_pieces(bits, lgb, prefix != nullptr);
+  const int km = keys == nullptr ? kKmInline : (flags & GCX_F_KEY_PREFIX) ? kKmPrefix : kKmTable;
+  SpanPiecesFn fn = pick_pieces(bits, lgb, km);
   if (fn == nullptr) return cudaErrorInvalidValue;
   const size_t smem = size_t(kWarps) * warp_smem_bytes(uint32_t(bits) + 1);
-  static thread_local int occ[9][8][2] = {};
-  int& o = occ[bits][lgb][prefix != nullptr];
+  static thread_local int occ[9][8][3] = {};
+  int& o = occ[bits][lgb][km];
   if (o == 0) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
@@ -1265,7 +1293,7 @@ cudaError_t gcx_span_encode_pieces(const gcx_piece* pieces, const uint32_t* tile
   a.seed = seed;
   a.src = src;
   a.msg = msg;
-  a.keys = reinterpret_cast<const uint32_t*>(prefix);
+  a.keys = reinterpret_cast<const uint32_t*>(keys);
   a.bad = bad;
   uint32_t grid = (ntiles + kWarps - 1) / kWarps;
   if (grid > uint32_t(sms * o)) grid = uint32_t(sms * o);

@@ -29,8 +29,9 @@ cudaError_t gcx_span_decode_pieces(const gcx_piece* pieces, const uint32_t* tile
                                    uint32_t npieces, uint32_t ntiles, const uint8_t* msg,
                                    float* dst, float divisor, int sms, cudaStream_t st);
 // K1 span over a piece table with GCX_F_SPAN_ENC (bits and log2 bucket in the
-// flags); prefix == nullptr: keys hashed inline, else span-layout prefixes
+// flags); keys == nullptr: hashed inline; with GCX_F_KEY_PREFIX span-layout
+// prefixes, else a span-layout key table for this seed
 cudaError_t gcx_span_encode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix,
                                    uint32_t npieces, uint32_t ntiles, uint32_t flags, uint64_t seed,
-                                   const float* src, uint8_t* msg, const unsigned long long* prefix,
+                                   const float* src, uint8_t* msg, const unsigned long long* keys,
                                    unsigned long long* bad, int sms, cudaStream_t st);

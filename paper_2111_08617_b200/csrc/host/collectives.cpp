@@ -244,6 +244,9 @@ namespace {
 
 // A device piece table with its tile prefix (and, for tables quantized under
 // one seed, its key-table plan), uploaded into one blob.
+struct Table;
+bool onestep_table(const Table& t);
+
 struct Table {
   std::vector<gcx_piece> pieces;
   std::vector<std::uint32_t> prefix;
@@ -264,13 +267,26 @@ struct Table {
     key_len = 0;
     for (auto& p : pieces) p.keys = ~0ULL;
     if (with_keys && !pieces.empty()) {
-      groups.resize(pieces.size());
-      std::uint32_t ng = 0;
-      const std::int64_t len = gcx_plan_keys(pieces.data(), std::uint32_t(pieces.size()),
-                                             groups.data(), std::uint32_t(groups.size()), &ng);
-      if (len < 0) gcx_check(int(len));
-      groups.resize(ng);
-      key_len = std::uint64_t(len);
+      auto plan_keys = [&](int layout) {
+        groups.resize(pieces.size());
+        std::uint32_t ng = 0;
+        const std::int64_t len =
+            gcx_plan_keys_layout(pieces.data(), std::uint32_t(pieces.size()), groups.data(),
+                                 std::uint32_t(groups.size()), &ng, layout);
+        if (len < 0) gcx_check(int(len));
+        groups.resize(ng);
+        key_len = std::uint64_t(len);
+      };
+      plan_keys(GCX_KEYS_AUTO);
+      // The span K1 wins when it hashes straight from the prefixes (one
+      // launch: an unshared, large key table — an owner chunk, N = 2's peer
+      // chunk); tables whose key slots are read by several pieces (N > 2
+      // stage 1) keep the two-step key table + CTA K1, so they take the
+      // lane-group layout and drop GCX_F_SPAN_ENC.
+      if ((flags & GCX_F_SPAN_ENC) && !onestep_table(*this)) {
+        flags &= ~(GCX_F_SPAN_ENC | (0xFFu << GCX_F_SPAN_BITS_SHIFT));
+        plan_keys(GCX_KEYS_LANE_GROUP);
+      }
     }
   }
 };
@@ -337,17 +353,12 @@ bool onestep(const Table& t) {
   return t.key_len >= onestep_min_slots() && 2 * q < 3 * t.key_len;
 }
 
+bool onestep_table(const Table& t) { return onestep(t); }
+
 void encode(const TableBlob& blob, const Table& t, std::uint64_t seed, const float* src,
             std::uint8_t* msg, unsigned long long* keys, unsigned long long* bad,
             cudaStream_t st, const unsigned long long* key_prefix = nullptr) {
   const bool use_keys = keys != nullptr && t.key_len > 0;
-  if (t.flags & GCX_F_SPAN_ENC) {  // span K1: one launch, from the prefixes or hashing inline
-    const bool pre = use_keys && key_prefix != nullptr;
-    gcx_check(gcx_encode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
-                                t.ntiles, t.flags | (pre ? GCX_F_KEY_PREFIX : 0u), seed, src, msg,
-                                pre ? key_prefix : nullptr, bad, st));
-    return;
-  }
   if (use_keys && key_prefix != nullptr && onestep(t)) {
     gcx_check(gcx_encode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
                                 t.ntiles, t.flags | GCX_F_KEY_PREFIX, seed, src, msg, key_prefix,
