@@ -348,7 +348,7 @@ def run_codec(args):
     achieved = q_bytes / (q_ms * 1e-3) / 1e9
     cb = cpu_codec_sample(reps=3)
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "round1_c1_k_quant32.json")
+    tp = os.path.join(ROOT, "profiles", "round2_c1_k_span.json")
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("bytes_per_launch")
@@ -381,26 +381,34 @@ def run_codec(args):
                               "per element), once per step inside observation windows",
                    "quantize_GBps_algorithmic": achieved,
                    "dequantize_GBps_algorithmic": q_bytes / (dq_ms * 1e-3) / 1e9,
+                   "dequantize_roofline_frac": q_bytes / (dq_ms * 1e-3) / 1e9 / peak,
+                   "dequantize_kernel": "k_dspan<4,7> (K3: per-lane shuffle tables, "
+                                        "coalesced 16-byte streaming stores; "
+                                        "profiles/round2_c1_k_dspan.md)",
                    "hash_only_ms": {f"variant{k}": v for k, v in hash_ms.items()},
                    "hash_only_Gdraws_per_s": n / (min(hash_ms.values()) * 1e-3) / 1e9},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_quant32 (K1: fused bucket norms + stochastic quantize + pack, "
-                               "one launch per gcx_quantize)", "peak_kind": peak_kind,
-                     "note": "K1 is bound by the reference RNG's integer work and its latency, "
-                             "not HBM: with the key prefixes it hashes one SplitMix64 finalizer "
-                             "per element and reads the 8-byte prefix T(i) (traffic ~ 4+8 B/elem "
-                             "vs 4.6 algorithmic); ncu (profiles/round1_c1_k_quant32.md): issue "
-                             "slots 45 % busy, ALU pipe 48 %, long-scoreboard the top stall at "
-                             "25 % occupancy (128 registers); config.hash_only_ms is the "
-                             "three-finalizer hash alone (the inline path's ceiling)",
+                     "kernel": "k_span<4,7,prefix> (K1: lane-per-128-element rows staged by "
+                               "2-D TMA into swizzled shared slots, fused sequential FP64 norms, "
+                               "one SplitMix64 finalizer per element from the key prefixes, "
+                               "register bit-packing, bulk-stored words; one launch per "
+                               "gcx_quantize_prefixed)", "peak_kind": peak_kind,
+                     "note": "K1 is bound by instruction issue and latency, not HBM: ~43 "
+                             "instructions per element (the reference RNG's finalizer ~18, "
+                             "exact FP64 level arithmetic, packing) at 2 warps per scheduler "
+                             "(216 registers); it reads the 8-byte prefix T(i) per element "
+                             "(traffic ~ 4+8 B/elem vs 4.66 algorithmic).  The bit-exact "
+                             "contract (SURVEY Appendix B) rules out skipping the hash; "
+                             "config.hash_only_ms is the three-finalizer hash alone.  ncu: "
+                             "profiles/round2_c1_k_span.md",
                      "algorithmic_bytes_per_launch": q_bytes},
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
                                             "cpu_model")},
         "e2e": {"value": 4 * n / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
                 "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
                 "path": "pinned H2D -> gcx_quantize_prefixed -> gcx_dequantize -> D2H, steps double-buffered over copy-in / compute / copy-out streams"},
-        "gpu_launches": 2 * args.steps,  # k_quant32 + k_decode32 per step
+        "gpu_launches": 2 * args.steps,  # k_span + k_dspan per step
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

@@ -1,14 +1,16 @@
 #!/bin/bash
 # GPU call: parity suite, smoke, bench line (ours + reference arm), launch
-# list, and the K3 ncu capture (K1's capture is ~53 MB: take it in its own
-# call, see profiles/README.md)
+# list, ncu captures of the two C1 kernels (K1 k_span, K3 k_dspan) and the
+# per-kernel launch list of one emulated N = 8 SRA step
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
 nproc > gpurun_out/nproc.txt; lscpu | head -20 >> gpurun_out/nproc.txt
-timeout 1200 python -m pytest tests -m gpu -q -x --timeout=300 --durations=10 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout=300 --durations=10 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 400 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 400 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 > /dev/null 2>&1
-timeout 400 ncu --set full --clock-control none --import-source on -k regex:k_decode32 -s 2 -c 1 -o gpurun_out/c1_k_decode32 python bench.py --steps 2 --warmup 3 > gpurun_out/ncu_c1_k_decode32.log 2>&1
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:k_span -s 2 -c 1 -o gpurun_out/c1_k_span python bench.py --steps 2 --warmup 3 > /dev/null 2>&1
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:k_dspan -s 2 -c 1 -o gpurun_out/c1_k_dspan python bench.py --steps 2 --warmup 3 > /dev/null 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/sra8_launches.csv python scripts/sra_emul_profile.py 8 > /dev/null 2>&1
 tail -4 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err; cat gpurun_out/bench_ref.json; ls gpurun_out

@@ -1,5 +1,5 @@
 """Summarise an ncu --set full capture (.ncu-rep) into a small markdown /
-json pair under profiles/.  Usage: python scripts/ncu_summary.py REP NAME"""
+json pair under profiles/ (or OUTDIR).  Usage: python scripts/ncu_summary.py REP NAME [OUTDIR]"""
 import csv
 import io
 import json
@@ -18,7 +18,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 
 
-def main(rep, name):
+def main(rep, name, outdir="profiles"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -34,8 +34,8 @@ def main(rep, name):
     rd = float(d["dram__bytes_read.sum"]) * (1e6 if u.get("dram__bytes_read.sum") == "Mbyte" else 1)
     wr = float(d["dram__bytes_write.sum"]) * (1e6 if u.get("dram__bytes_write.sum") == "Mbyte" else 1)
     out["bytes_per_launch"] = rd + wr
-    json.dump(out, open(f"profiles/{name}.json", "w"), indent=1)
-    with open(f"profiles/{name}.md", "w") as f:
+    json.dump(out, open(f"{outdir}/{name}.json", "w"), indent=1)
+    with open(f"{outdir}/{name}.md", "w") as f:
         f.write(f"# {name}: ncu --set full summary\n\nkernel: `{out['kernel']}`\n\n")
         for k in KEYS:
             f.write(f"- {k} = {d.get(k)} {u.get(k, '')}\n")
@@ -47,4 +47,4 @@ def main(rep, name):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(*sys.argv[1:4])
