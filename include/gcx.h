@@ -172,6 +172,17 @@ int gcx_decode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint
 int gcx_fold_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
                     uint32_t ntiles, uint32_t flags, const uint8_t* recv, uint64_t slot_stride,
                     const float* own, uint32_t nodes, uint32_t me, float* out, void* stream);
+/* fold_encode: the owner's fold and hop-1 re-encode in one pass
+ * (collectives.cpp:266-284): the aggregate goes straight into bcast, never
+ * to HBM.  One launch when the table qualifies (GCX_F_SPAN_ENC, bits <= 4,
+ * bucket 128, nodes <= 8; keys = the table's span-layout prefixes with
+ * GCX_F_KEY_PREFIX, or NULL to hash inline), else fold into out and encode
+ * out (keys as gcx_encode_pieces). */
+int gcx_sra_fold_encode(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
+                        uint32_t ntiles, uint32_t flags, const uint8_t* recv, uint64_t slot_stride,
+                        const float* own, uint32_t nodes, uint32_t me, uint64_t seed,
+                        uint8_t* bcast, float* out, const unsigned long long* keys,
+                        unsigned long long* bad_key, void* stream);
 int gcx_sra_reduce(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
                    uint32_t ntiles, uint32_t flags, const uint8_t* recv, uint64_t slot_stride,
                    const float* own, uint32_t nodes, uint32_t me, uint64_t seed,

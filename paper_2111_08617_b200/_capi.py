@@ -84,6 +84,8 @@ _decl("gcx_make_keys", i32, vp, u32, u64, u64, vp, vp)
 _decl("gcx_make_key_prefix", i32, vp, u32, u64, vp, vp)
 _decl("gcx_make_keys_prefixed", i32, u64, u64, vp, vp, vp)
 _decl("gcx_fold_pieces", i32, vp, vp, u32, u32, u32, vp, u64, vp, u32, u32, vp, vp)
+_decl("gcx_sra_fold_encode", i32, vp, vp, u32, u32, u32, vp, u64, vp, u32, u32, u64, vp, vp, vp,
+      vp, vp)
 _decl("gcx_sra_reduce", i32, vp, vp, u32, u32, u32, vp, u64, vp, u32, u32, u64, vp, vp,
       C.c_float, vp, vp, vp)
 _decl("gcx_hash_bench", i32, u64, u64, u32, i32, vp, vp)
@@ -97,7 +99,7 @@ _decl("gcx_device_info", i32, i32, C.POINTER(i32), C.POINTER(i32))
 EXPORTS = ["gcx_version", "gcx_last_error", "gcx_compressed_size", "gcx_packed_bytes",
            "gcx_packed_capacity", "gcx_hop_seed", "gcx_uniform01", "gcx_plan_tiles",
            "gcx_quantize", "gcx_dequantize", "gcx_encode_pieces", "gcx_decode_pieces",
-           "gcx_sra_reduce", "gcx_hash_bench", "gcx_device_info", "gcx_plan_keys",
+           "gcx_sra_reduce", "gcx_sra_fold_encode", "gcx_hash_bench", "gcx_device_info", "gcx_plan_keys",
            "gcx_make_keys", "gcx_fold_pieces", "gcx_prefix_slots", "gcx_make_prefix",
            "gcx_quantize_prefixed", "gcx_make_key_prefix", "gcx_make_keys_prefixed",
            "gcx_stats_accumulate", "gcx_add_f32", "gcx_wire_layout", "gcx_frame_pieces",

@@ -539,11 +539,113 @@ struct SpanPiecesArgs {
   gcx_plan::PlanView pv;
   uint32_t flags;
   uint64_t seed;
-  const float* src;
-  uint8_t* msg;
+  const float* src;      // the input (FOLD: the owner's raw values)
+  uint8_t* msg;          // the message written (FOLD: the owner's broadcast message)
   const uint32_t* keys;  // span-layout prefix words or nullptr (inline)
   unsigned long long* bad;
+  // FOLD (SRA owner step): peer id's message for this chunk sits in receive
+  // slot (id < me ? id : id - 1) at recv + slot * slot_stride
+  const uint8_t* recv;
+  uint64_t slot_stride;
+  uint32_t nodes, me;
 };
+
+// The SRA owner's fold of one tile (collectives.cpp:266-279) straight into
+// the K1 staging slots: row r of the tile (one bucket of 128) is decoded from
+// every peer's payload warp-wide — lane l owns elements 4l..4l+3, the peer's
+// table for the row's bucket lives one entry per lane (as k_dspan), so a
+// value is one shuffle — and added in ascending node id with the owner's raw
+// values (f32, the reference's order).  The aggregate is stored swizzled into
+// slot l/8, where the span K1 passes read it.  Row r+1's loads (the peers'
+// norms and packed windows, the owner's raw quad) are issued before row r is
+// folded.  Requires bits <= 4 and bucket 128; nodes <= 8.
+template <uint32_t BITS>
+__device__ __forceinline__ void fold_tile(const SpanPiecesArgs& A, const gcx_piece& p,
+                                          uint32_t start, uint32_t count, float* slots,
+                                          uint32_t lane, uint32_t r0 = 0, uint32_t r1 = 32) {
+  constexpr uint32_t W = BITS + 1, S = (1u << BITS) - 1, F = 2u << BITS;
+  const uint32_t f = lane & (F - 1u), level = f & S, sign = f >> BITS;
+  const double dl = double(level);
+  const double sd = double(S), ys = __drcp_rn(sd);
+  const uint32_t qbit = 4 * W * lane, qw = qbit >> 5, qsh = qbit & 31u;
+  const bool two = qsh + 4 * W > 32;
+  const uint32_t nodes = A.nodes, me = A.me;
+  struct RowLoads {
+    uint32_t nu[8], w0[8], w1[8];
+    float4 own;
+  };
+  auto load_row = [&](uint32_t r, RowLoads& L) {
+    const uint32_t vr = count > r * 128u ? min(128u, count - r * 128u) : 0u;
+    const uint32_t e_row = start + r * 128u;
+    const bool quad = 4 * lane < vr;
+    L.own = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (quad) {
+      const float* o = A.src + p.src + e_row + 4 * lane;
+      if (4 * lane + 4 <= vr && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
+        L.own = __ldg(reinterpret_cast<const float4*>(o));
+      } else {
+        L.own.x = __ldg(o);
+        if (4 * lane + 1 < vr) L.own.y = __ldg(o + 1);
+        if (4 * lane + 2 < vr) L.own.z = __ldg(o + 2);
+        if (4 * lane + 3 < vr) L.own.w = __ldg(o + 3);
+      }
+    }
+#pragma unroll
+    for (uint32_t id = 0; id < 8; ++id) {
+      L.nu[id] = 0u;
+      L.w0[id] = 0u;
+      L.w1[id] = 0u;
+      if (id < nodes && id != me && vr > 0) {
+        const uint8_t* m = A.recv + uint64_t(id < me ? id : id - 1) * A.slot_stride;
+        L.nu[id] = __ldg(reinterpret_cast<const uint32_t*>(m + p.norms) + (e_row >> 7));
+        if (quad) {
+          const uint32_t* wp = reinterpret_cast<const uint32_t*>(m + p.packed) + (e_row >> 5) * W + qw;
+          L.w0[id] = __ldg(wp);
+          if (two) L.w1[id] = __ldg(wp + 1);
+        }
+      }
+    }
+  };
+  RowLoads cur;
+  load_row(r0, cur);
+#pragma unroll 1
+  for (uint32_t r = r0; r < r1; ++r) {
+    RowLoads nxt;
+    if (r + 1 < r1) load_row(r + 1, nxt);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (uint32_t id = 0; id < 8; ++id) {
+      if (id >= nodes) break;
+      float x[4];
+      if (id == me) {
+        x[0] = cur.own.x;
+        x[1] = cur.own.y;
+        x[2] = cur.own.z;
+        x[3] = cur.own.w;
+      } else {
+        // this lane's entry of peer id's table for the row's bucket (dequant_field)
+        const double nl = __dmul_rn(double(__uint_as_float(cur.nu[id])), dl);  // exact
+        const double q0 = __dmul_rn(nl, ys);
+        const double q = __fma_rn(__fma_rn(-sd, q0, nl), ys, q0);
+        const float m = __double2float_rn(q);
+        const float entry = level == 0 ? 0.0f : (sign ? -m : m);
+        const uint32_t win = two ? __funnelshift_r(cur.w0[id], cur.w1[id], qsh) : (cur.w0[id] >> qsh);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = __shfl_sync(0xffffffffu, entry, (win >> (k * W)) & (F - 1u));
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] = id == 0 ? x[k] : __fadd_rn(acc[k], x[k]);
+    }
+    // elements past the piece stay 0 (zero-filled tile)
+    const uint32_t vr = count > r * 128u ? min(128u, count - r * 128u) : 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (4 * lane + k >= vr) acc[k] = 0.0f;
+    float* dst = slots + (lane >> 3) * kSlotFloats + r * 32u + ((((lane & 7u) ^ (r & 7u))) << 2);
+    *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    cur = nxt;
+  }
+}
 
 __device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
@@ -559,8 +661,9 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <uint32_t BITS, int LGB, int KM>
+template <uint32_t BITS, int LGB, int KM, bool FOLD>
 __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A) {
+  static_assert(!FOLD || (BITS <= 4 && LGB == 7), "the fused fold needs bits <= 4 and bucket 128");
   constexpr uint32_t W = BITS + 1;
   constexpr uint32_t BL = 1u << LGB;
   constexpr uint32_t NB = kSpan / BL;
@@ -606,6 +709,7 @@ __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A
   };
   // quarter Q = quarter Q % 4 of this warp's (Q / 4)-th tile, slot Q % 5
   auto issue = [&](uint32_t Q) {
+    if (FOLD) return;  // the fold writes the slots itself
     const uint32_t t = gw + (Q >> 2) * nw, g = Q & 3u;
     if (t >= ntiles) return;
     gcx_plan::TileCtx c;
@@ -660,7 +764,22 @@ __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A
     if (p.bits == 0) {  // raw piece: its f32 values are the payload (collectives.cpp:153-158)
       const float* xs = A.src + p.src + cur.start;
       float* d = reinterpret_cast<float*>(A.msg + p.norms) + cur.start;
-      for (uint32_t e = lane; e < cur.count; e += 32) d[e] = __ldcs(xs + e);
+      if (FOLD) {  // the raw fold, ascending id (collectives.cpp:268-279)
+        for (uint32_t e = lane; e < cur.count; e += 32) {
+          float acc = 0.0f;
+          for (uint32_t id = 0; id < A.nodes; ++id) {
+            const float x =
+                id == A.me ? __ldg(xs + e)
+                           : __ldg(reinterpret_cast<const float*>(
+                                 A.recv + uint64_t(id < A.me ? id : id - 1) * A.slot_stride + p.norms) +
+                                 cur.start + e);
+            acc = id == 0 ? x : __fadd_rn(acc, x);
+          }
+          d[e] = acc;
+        }
+      } else {
+        for (uint32_t e = lane; e < cur.count; e += 32) d[e] = __ldcs(xs + e);
+      }
       if (KM != kKmInline && more && nxt.p.bits > 0) {  // the key ring's next group
         const uint4* kn = key_group(nxt, 0);
 #pragma unroll
@@ -685,8 +804,12 @@ __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A
     const unsigned long long pkey = uint64_t(cur.pidx) << 40;
     RowView rv;
 #pragma unroll
-    for (uint32_t g = 0; g < 4; ++g) rv.slot[g] = slots + ((4 * j + g) % kSlots) * kSlotFloats;
+    for (uint32_t g = 0; g < 4; ++g) rv.slot[g] = slots + (FOLD ? g : (4 * j + g) % kSlots) * kSlotFloats;
     rv.r = lane;
+    if (FOLD) {
+      if constexpr (FOLD) fold_tile<BITS>(A, p, cur.start, cur.count, slots, lane);
+      __syncwarp();
+    }
 
     // ---- pass 1 ----
     uint32_t nu[NB];
@@ -695,7 +818,7 @@ __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A
       double sq = 0.0;
 #pragma unroll
       for (uint32_t g = 0; g < 4; ++g) {
-        wait_q(4 * j + g);
+        if (!FOLD) wait_q(4 * j + g);
         const float* row = rv.slot[g] + lane * 32u;
 #pragma unroll
         for (uint32_t q = 0; q < 8; ++q) {
@@ -755,7 +878,7 @@ __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A
         }
       const uint32_t i0 = i_lane + g * 32;
       const uint4* kn = g < 3 ? kp + (g + 1) * 512 : kp_next;
-      const float* slot = slots + ((4 * j + g) % kSlots) * kSlotFloats;
+      const float* slot = rv.slot[g];
       uint32_t* wout = outw + (lane * 4 + g) * W;
       uint32_t w[W];
       const bool ok = span_group_fast<BITS, LGB, KM>(slot, lane, i0, nug, s_lo, s_hi, shk, w, kh,
@@ -1233,14 +1356,181 @@ cudaError_t gcx_span_decode_pieces(const gcx_piece* pieces, const uint32_t* tile
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Fused SRA owner step, CTA per tile (k_span_fold_cta): the owner's chunk is
+// 1/N of a buffer (476 tiles for ResNet-50 buffer 0 at N = 8), too few tiles
+// for one warp per tile to hide the fold's latency, so the four warps of a CTA
+// share each tile:
+//   A  warp w folds rows 8w..8w+7 into the swizzled slots (fold_tile);
+//   B  warp 0: the sequential FP64 norms, lane per row; warps 1-3 load keys;
+//   C  warp w quantizes group w (elements [32w, 32w+32)) of every row;
+//   D  the tile's packed words leave with one bulk store.
+// ---------------------------------------------------------------------------
+constexpr int kFoldWarps = 4;
+
+template <uint32_t BITS, int KM>
+__global__ void __launch_bounds__(32 * kFoldWarps, 1) k_span_fold_cta(SpanPiecesArgs A) {
+  constexpr uint32_t W = BITS + 1;
+  extern __shared__ __align__(1024) unsigned char span_smem[];
+  float* slots = reinterpret_cast<float*>(span_smem);                       // 4 x 4 KB
+  uint32_t* outw = reinterpret_cast<uint32_t*>(span_smem + 4 * kSlotFloats * 4);  // 128 W
+  uint32_t* nus = outw + out_words(W);                                      // 32 norms
+  uint32_t* cars = nus + 32;                                                 // 32 flags
+  __shared__ gcx_plan::TileCtx ctx_s;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const HashK shk = make_hashk();
+  const uint32_t s_lo = uint32_t(A.seed), s_hi = uint32_t(A.seed >> 32);
+  for (uint32_t t = blockIdx.x; t < A.pv.ntiles; t += gridDim.x) {
+    if (warp == 0) {
+      gcx_plan::TileCtx c;
+      gcx_plan::locate_warp(A.pv, t, c);
+      if (lane == 0) ctx_s = c;
+    }
+    __syncthreads();
+    const gcx_plan::TileCtx cur = ctx_s;
+    const gcx_piece& p = cur.p;
+    if (p.bits == 0) {  // raw piece: the raw fold, ascending id (collectives.cpp:268-279)
+      const float* xs = A.src + p.src + cur.start;
+      float* d = reinterpret_cast<float*>(A.msg + p.norms) + cur.start;
+      for (uint32_t e = threadIdx.x; e < cur.count; e += 32 * kFoldWarps) {
+        float acc = 0.0f;
+        for (uint32_t id = 0; id < A.nodes; ++id) {
+          const float x =
+              id == A.me ? __ldg(xs + e)
+                         : __ldg(reinterpret_cast<const float*>(
+                               A.recv + uint64_t(id < A.me ? id : id - 1) * A.slot_stride + p.norms) +
+                               cur.start + e);
+          acc = id == 0 ? x : __fadd_rn(acc, x);
+        }
+        d[e] = acc;
+      }
+      __syncthreads();
+      continue;
+    }
+    // A: fold
+    fold_tile<BITS>(A, p, cur.start, cur.count, slots, lane, 8 * warp, 8 * warp + 8);
+    __syncthreads();
+    RowView rv;
+#pragma unroll
+    for (uint32_t g = 0; g < 4; ++g) rv.slot[g] = slots + g * kSlotFloats;
+    rv.r = lane;
+    const uint32_t i_lane = cur.start + lane * kSpan;
+    // B: norms (warp 0), keys (every warp, its group)
+    uint4 kh[8], kl[8];
+    const uint4* kg = KM != kKmInline ? reinterpret_cast<const uint4*>(A.keys) +
+                                            ((p.keys + cur.start) >> 12) * 2048 + warp * 512 + lane
+                                      : nullptr;
+    if (KM != kKmInline) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        kh[q] = __ldg(kg + q * 32);
+        if (KM == kKmPrefix) kl[q] = __ldg(kg + 256 + q * 32);
+      }
+    }
+    if (warp == 0) {
+      double sq = 0.0;
+#pragma unroll
+      for (uint32_t g = 0; g < 4; ++g) {
+        const float* row = rv.slot[g] + lane * 32u;
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q) {
+          const float4 v = *reinterpret_cast<const float4*>(row + ((q ^ (lane & 7u)) << 2));
+          double d = double(v.x);
+          sq = __fma_rn(d, d, sq);
+          d = double(v.y);
+          sq = __fma_rn(d, d, sq);
+          d = double(v.z);
+          sq = __fma_rn(d, d, sq);
+          d = double(v.w);
+          sq = __fma_rn(d, d, sq);
+        }
+      }
+      const bool c = (uint32_t(__double2hiint(sq)) & 0x7FF00000u) == 0x7FF00000u;
+      uint32_t v;
+      if (c) {
+        v = span_norm_exact(rv, 0, 128, 0u, nullptr);
+        if (A.bad != nullptr)
+          for (uint32_t e = 0; e < 128; ++e)
+            if ((__float_as_uint(rv.at(e)) & 0x7FFFFFFFu) >= 0x7F800000u) {
+              atomicMin(A.bad, (uint64_t(cur.pidx) << 40) | (i_lane + e));
+              break;
+            }
+      } else {
+        v = __float_as_uint(__double2float_rn(__dsqrt_rn(sq)));
+      }
+      nus[lane] = v;
+      cars[lane] = c ? 1u : 0u;
+      if (i_lane < p.len) reinterpret_cast<uint32_t*>(A.msg + p.norms)[i_lane >> 7] = v;
+      if (lane == 0) bulk_wait_read0();  // the previous tile's bulk store has read outw
+    }
+    __syncthreads();
+    // C: group `warp` of every row
+    {
+      const uint32_t g = warp;
+      const uint32_t nug = nus[lane];
+      const bool car = cars[lane] != 0u;
+      const uint32_t i0 = i_lane + g * 32;
+      uint32_t* wout = outw + (lane * 4 + g) * W;
+      uint32_t w[W];
+      const bool ok = span_group_fast<BITS, 7, KM>(rv.slot[g], lane, i0, nug, s_lo, s_hi, shk, w, kh,
+                                                   kl, nullptr) &&
+                      nug != 0u && !car;
+      if (ok) {
+#pragma unroll
+        for (int m = 0; m < int(W); ++m) wout[m] = w[m];
+      } else {
+        span_group_exact<BITS, 7, KM>(
+            rv, g, i0, nug, A.seed,
+            KM != kKmInline ? A.keys + ((p.keys + cur.start) >> 12) * 8192u : nullptr, lane, wout);
+      }
+    }
+    __syncthreads();
+    // D: the packed words
+    uint32_t* dstw = reinterpret_cast<uint32_t*>(A.msg + p.packed) + uint64_t(cur.start >> 5) * W;
+    if (cur.count == kWTile && (reinterpret_cast<uintptr_t>(dstw) & 15u) == 0) {
+      if (threadIdx.x == 0) {
+        fence_async_smem();
+        bulk_s2g(dstw, outw, out_words(W) * 4);
+      }
+    } else {
+      const uint32_t nwords = (cur.count * W + 31) / 32;
+      for (uint32_t e = threadIdx.x; e < nwords; e += 32 * kFoldWarps) dstw[e] = outw[e];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bulk_wait0();
+}
+
 using SpanPiecesFn = void (*)(SpanPiecesArgs);
 
 template <uint32_t BITS, int LGB>
 SpanPiecesFn pick_pieces_km(int km) {
   switch (km) {
-    case kKmTable: return k_span_pieces<BITS, LGB, kKmTable>;
-    case kKmPrefix: return k_span_pieces<BITS, LGB, kKmPrefix>;
-    default: return k_span_pieces<BITS, LGB, kKmInline>;
+    case kKmTable: return k_span_pieces<BITS, LGB, kKmTable, false>;
+    case kKmPrefix: return k_span_pieces<BITS, LGB, kKmPrefix, false>;
+    default: return k_span_pieces<BITS, LGB, kKmInline, false>;
+  }
+}
+
+#ifndef GCX_FOLD_CTA
+#define GCX_FOLD_CTA 1  // the fused owner step: 1 = CTA per tile, 0 = warp per tile
+#endif
+static SpanPiecesFn pick_fold(int bits, bool prefix) {
+  if (GCX_FOLD_CTA) {
+    switch (bits) {
+      case 1: return prefix ? k_span_fold_cta<1, kKmPrefix> : k_span_fold_cta<1, kKmInline>;
+      case 2: return prefix ? k_span_fold_cta<2, kKmPrefix> : k_span_fold_cta<2, kKmInline>;
+      case 3: return prefix ? k_span_fold_cta<3, kKmPrefix> : k_span_fold_cta<3, kKmInline>;
+      case 4: return prefix ? k_span_fold_cta<4, kKmPrefix> : k_span_fold_cta<4, kKmInline>;
+      default: return nullptr;
+    }
+  }
+  switch (bits) {
+    case 1: return prefix ? k_span_pieces<1, 7, kKmPrefix, true> : k_span_pieces<1, 7, kKmInline, true>;
+    case 2: return prefix ? k_span_pieces<2, 7, kKmPrefix, true> : k_span_pieces<2, 7, kKmInline, true>;
+    case 3: return prefix ? k_span_pieces<3, 7, kKmPrefix, true> : k_span_pieces<3, 7, kKmInline, true>;
+    case 4: return prefix ? k_span_pieces<4, 7, kKmPrefix, true> : k_span_pieces<4, 7, kKmInline, true>;
+    default: return nullptr;
   }
 }
 
@@ -1295,9 +1585,61 @@ cudaError_t gcx_span_encode_pieces(const gcx_piece* pieces, const uint32_t* tile
   a.msg = msg;
   a.keys = reinterpret_cast<const uint32_t*>(keys);
   a.bad = bad;
+  a.recv = nullptr;
+  a.slot_stride = 0;
+  a.nodes = 0;
+  a.me = 0;
   uint32_t grid = (ntiles + kWarps - 1) / kWarps;
   if (grid > uint32_t(sms * o)) grid = uint32_t(sms * o);
   if (grid == 0) grid = 1;
   fn<<<grid, 32 * kWarps, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+bool gcx_span_fold_ok(uint32_t flags, uint32_t nodes) {
+  const uint32_t bits = (flags >> GCX_F_SPAN_BITS_SHIFT) & 15u;
+  const uint32_t lgb = (flags >> GCX_F_SPAN_LGB_SHIFT) & 15u;
+  return (flags & GCX_F_SPAN_ENC) && bits >= 1 && bits <= 4 && lgb == 7 && nodes >= 2 && nodes <= 8;
+}
+
+cudaError_t gcx_span_fold_encode(const gcx_piece* pieces, const uint32_t* tile_prefix,
+                                 uint32_t npieces, uint32_t ntiles, uint32_t flags,
+                                 const uint8_t* recv, uint64_t slot_stride, const float* own,
+                                 uint32_t nodes, uint32_t me, uint64_t seed, uint8_t* bcast,
+                                 const unsigned long long* prefix, unsigned long long* bad, int sms,
+                                 cudaStream_t st) {
+  if (!gcx_span_fold_ok(flags, nodes) || me >= nodes) return cudaErrorInvalidValue;
+  const int bits = int((flags >> GCX_F_SPAN_BITS_SHIFT) & 15u);
+  SpanPiecesFn fn = pick_fold(bits, prefix != nullptr);
+  if (fn == nullptr) return cudaErrorInvalidValue;
+  const uint32_t W = uint32_t(bits) + 1;
+  const size_t smem = GCX_FOLD_CTA ? size_t(4 * kSlotFloats * 4 + out_words(W) * 4 + 64 * 4)
+                                   : size_t(kWarps) * warp_smem_bytes(W);
+  const int threads = GCX_FOLD_CTA ? 32 * kFoldWarps : 32 * kWarps;
+  static thread_local int occ[9][2] = {};
+  int& o = occ[bits][prefix != nullptr];
+  if (o == 0) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (o < 1) o = 1;
+  }
+  SpanPiecesArgs a;
+  a.pv = gcx_plan::PlanView{pieces, tile_prefix, npieces, ntiles, {}};
+  a.flags = flags | (prefix != nullptr ? GCX_F_KEY_PREFIX : 0u);
+  a.seed = seed;
+  a.src = own;
+  a.msg = bcast;
+  a.keys = reinterpret_cast<const uint32_t*>(prefix);
+  a.bad = bad;
+  a.recv = recv;
+  a.slot_stride = slot_stride;
+  a.nodes = nodes;
+  a.me = me;
+  uint32_t grid = GCX_FOLD_CTA ? ntiles : (ntiles + kWarps - 1) / kWarps;
+  if (grid > uint32_t(sms * o)) grid = uint32_t(sms * o);
+  if (grid == 0) grid = 1;
+  fn<<<grid, threads, smem, st>>>(a);
   return cudaGetLastError();
 }

@@ -35,3 +35,13 @@ cudaError_t gcx_span_encode_pieces(const gcx_piece* pieces, const uint32_t* tile
                                    uint32_t npieces, uint32_t ntiles, uint32_t flags, uint64_t seed,
                                    const float* src, uint8_t* msg, const unsigned long long* keys,
                                    unsigned long long* bad, int sms, cudaStream_t st);
+// Fused SRA owner step, fold + hop-1 re-encode (GCX_F_SPAN_ENC tables with
+// bits <= 4, bucket 128, 2 <= nodes <= 8); prefix: the table's span-layout key
+// prefixes, or nullptr to hash inline
+bool gcx_span_fold_ok(uint32_t flags, uint32_t nodes);
+cudaError_t gcx_span_fold_encode(const gcx_piece* pieces, const uint32_t* tile_prefix,
+                                 uint32_t npieces, uint32_t ntiles, uint32_t flags,
+                                 const uint8_t* recv, uint64_t slot_stride, const float* own,
+                                 uint32_t nodes, uint32_t me, uint64_t seed, uint8_t* bcast,
+                                 const unsigned long long* prefix, unsigned long long* bad, int sms,
+                                 cudaStream_t st);

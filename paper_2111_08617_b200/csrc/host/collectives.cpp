@@ -257,7 +257,9 @@ struct Table {
   std::vector<gcx_keygroup> groups;
   std::uint64_t key_len = 0;  // key-table entries this table needs
   std::size_t grp_off = 0;
-  void plan(bool with_keys = false) {
+  // with_keys: plan key runs; keep_span: keep the span key layout even when
+  // the table is not a one-step table (an owner table fed to the fused fold)
+  void plan(bool with_keys = false, bool keep_span = false) {
     prefix.assign(pieces.size() + 1, 0);
     const std::int64_t nt =
         gcx_plan_tiles(pieces.data(), std::uint32_t(pieces.size()), prefix.data(), &flags);
@@ -283,7 +285,7 @@ struct Table {
       // chunk); tables whose key slots are read by several pieces (N > 2
       // stage 1) keep the two-step key table + CTA K1, so they take the
       // lane-group layout and drop GCX_F_SPAN_ENC.
-      if ((flags & GCX_F_SPAN_ENC) && !onestep_table(*this)) {
+      if ((flags & GCX_F_SPAN_ENC) && !onestep_table(*this) && !keep_span) {
         flags &= ~(GCX_F_SPAN_ENC | (0xFFu << GCX_F_SPAN_BITS_SHIFT));
         plan_keys(GCX_KEYS_LANE_GROUP);
       }
@@ -373,6 +375,27 @@ void encode(const TableBlob& blob, const Table& t, std::uint64_t seed, const flo
   gcx_check(gcx_encode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
                               t.ntiles, t.flags, seed, src, msg, use_keys ? keys : nullptr, bad,
                               st));
+}
+
+// The owner's fold + hop-1 re-encode (collectives.cpp:266-284): one fused
+// launch when the table qualifies (gcx_sra_fold_encode: span K1 fed by the
+// fold, the aggregate never in HBM), else fold into `out` and encode it.
+void owner_step(const TableBlob& blob, const Table& t, const std::uint8_t* recv,
+                std::uint64_t slot_stride, const float* own, std::size_t nodes, std::size_t me,
+                std::uint64_t seed, std::uint8_t* bcast, float* out, unsigned long long* keys,
+                unsigned long long* bad, cudaStream_t st, const unsigned long long* key_prefix) {
+  const bool pre = key_prefix != nullptr && t.key_len > 0;
+  if ((t.flags & GCX_F_SPAN_ENC) && nodes <= 8) {
+    gcx_check(gcx_sra_fold_encode(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
+                                  t.ntiles, t.flags | (pre ? GCX_F_KEY_PREFIX : 0u), recv,
+                                  slot_stride, own, std::uint32_t(nodes), std::uint32_t(me), seed,
+                                  bcast, out, pre ? key_prefix : nullptr, bad, st));
+    return;
+  }
+  gcx_check(gcx_fold_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
+                            t.ntiles, t.flags, recv, slot_stride, own, std::uint32_t(nodes),
+                            std::uint32_t(me), out, st));
+  encode(blob, t, seed, out, bcast, keys, bad, st, key_prefix);
 }
 
 Table shifted(const std::vector<gcx_piece>& src, std::uint64_t delta) {
@@ -756,7 +779,7 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
     }
     own[id] = shifted(L.chunks[id].pieces, 0);
     send[id].plan(true);
-    own[id].plan(true);
+    own[id].plan(true, /*keep_span=*/true);
     dec[id].plan();
     flags |= send[id].flags | own[id].flags;
     key_len = std::max({key_len, send[id].key_len, own[id].key_len});
@@ -806,14 +829,10 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
            mail.get<std::uint8_t>(), kp, badp + id, st, kpre[2 * id].get<unsigned long long>());
   // owners: ascending-id fold into out, re-encode with the hop-1 seed
   for (std::size_t c = 0; c < N; ++c) {
-    gcx_check(gcx_fold_pieces(blob.pieces(own[c]), blob.prefix(own[c]),
-                              std::uint32_t(own[c].pieces.size()), own[c].ntiles, own[c].flags,
-                              mail.get<std::uint8_t>() + mbase[c], slot_stride[c],
-                              in.get<float>() + c * d, std::uint32_t(N), std::uint32_t(c),
-                              out.get<float>() + c * d, st));
-    encode(blob, own[c], hop_seed(req.step_seed, 1, c), out.get<float>() + c * d,
-           gather.get<std::uint8_t>() + L.gather_offset[c], kp, badp + N + c, st,
-           kpre[2 * c + 1].get<unsigned long long>());
+    owner_step(blob, own[c], mail.get<std::uint8_t>() + mbase[c], slot_stride[c],
+               in.get<float>() + c * d, N, c, hop_seed(req.step_seed, 1, c),
+               gather.get<std::uint8_t>() + L.gather_offset[c], out.get<float>() + c * d, kp,
+               badp + N + c, st, kpre[2 * c + 1].get<unsigned long long>());
   }
   // stage 2 (all-gather): everyone decodes every owner's bytes (own included)
   for (std::size_t id = 0; id < N; ++id)
@@ -1078,7 +1097,7 @@ DeviceReducer::DeviceReducer(Transport& transport, std::size_t d, std::vector<Se
   }
   I.own = shifted(layout_.chunks[me].pieces, 0);
   I.send.plan(true);
-  I.own.plan(true);
+  I.own.plan(true, /*keep_span=*/true);
   I.dec.plan();
   I.flags = I.send.flags | I.own.flags;
   I.blob.upload({&I.send, &I.own, &I.dec});
@@ -1145,12 +1164,9 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
   // K2: ascending-id fold into out, then re-encode with the hop-1 seed
   // (collectives.cpp:266-284)
   std::uint8_t* bcast = I.gather_buf.get<std::uint8_t>() + layout_.gather_offset[me];
-  gcx_check(gcx_fold_pieces(I.blob.pieces(I.own), I.blob.prefix(I.own),
-                            std::uint32_t(I.own.pieces.size()), I.own.ntiles, I.own.flags,
-                            I.recv_buf.get<std::uint8_t>(), I.recv_stride, in, std::uint32_t(N),
-                            std::uint32_t(me), out, st));
-  encode(I.blob, I.own, hop_seed(step_seed, 1, me), out, bcast, keys, bad + 1, st,
-         I.prefix_own.get<unsigned long long>());
+  owner_step(I.blob, I.own, I.recv_buf.get<std::uint8_t>(), I.recv_stride, in, N, me,
+             hop_seed(step_seed, 1, me), bcast, out, keys, bad + 1, st,
+             I.prefix_own.get<unsigned long long>());
   // round 2: variable-size all-gather of the owners' compressed aggregates
   // (collectives.cpp:289, :297)
   transport_.exchange(I.sends[1], I.recvs[1], st);
