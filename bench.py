@@ -153,6 +153,34 @@ def cpu_codec_sample(reps=3, threads=None):
             "cpu_model": cpu_model(), "seconds_per_step": t}
 
 
+def cpu_sra_sample(nodes, n=1 << 22, reps=3):
+    """The reference's own SRA allreduce (oracle/_ref: collectives::allreduce
+    over SimNet, one std::thread per node) — or the C restatement if _ref is
+    absent — timed on this host: one 4-bit/128 quantized segment of n floats
+    per node, average, step seed 7.  -> the same effective-busbw metric."""
+    from oracle import Oracle, RefOracle
+    o = Oracle()
+    xs = [o.normal_vector(n, o.hash_combine(0xC5, r), 1.0) for r in range(nodes)]
+    segs = [(0, n, 0, C1_BITS, C1_BUCKET)]
+    if RefOracle.available():
+        ref, kind = RefOracle(), "reference"
+        run = lambda: ref.allreduce(xs, segs, 7, True)  # noqa: E731
+    else:
+        kind = "port"
+        run = lambda: o.sra_allreduce(xs, segs, 7, True)  # noqa: E731
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": (4 * n / t) * 2 * (nodes - 1) / nodes / 1e9, "unit": "GB/s", "cores": nodes,
+            "kind": kind,
+            "sample": f"SRA allreduce (SimNet, {nodes} node threads), one 4b/128 segment of "
+                      f"{n} floats per node, average, median of {reps}",
+            "cpu_model": cpu_model(), "seconds_per_step": t}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -497,7 +525,7 @@ def e2e_codec(args, sets, n, bits, bucket):
 
 def run_sra(args):
     from paper_2111_08617_b200 import sra_bench
-    return sra_bench.run(args, METRIC, ClockSampler, measured_peaks, cpu_codec_sample)
+    return sra_bench.run(args, METRIC, ClockSampler, measured_peaks, cpu_sra_sample)
 
 
 def main():

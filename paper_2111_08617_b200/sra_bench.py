@@ -15,7 +15,7 @@ import statistics
 import time
 
 
-def run(args, metric, ClockSampler, measured_peaks, cpu_codec_sample):
+def run(args, metric, ClockSampler, measured_peaks, cpu_sra_sample):
     import torch
     import torch.distributed as dist
 
@@ -98,6 +98,11 @@ def run(args, metric, ClockSampler, measured_peaks, cpu_codec_sample):
     e2e_ms = float(te.item())
 
     busbw = lambda ms_: (4 * n / (ms_ * 1e-3)) * 2 * (world - 1) / world / 1e9  # noqa: E731
+    # the reference's CPU SRA on this host (rank 0 only, after the timed region)
+    cb = None
+    if rank == 0:
+        s = cpu_sra_sample(world)
+        cb = {k: s[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
     peak, peak_kind = measured_peaks()
     wire = car.wire_bytes_sent()
     dev_bytes = car.device_bytes_sent()
@@ -123,10 +128,14 @@ def run(args, metric, ClockSampler, measured_peaks, cpu_codec_sample):
                        "l2": "inputs refilled before every step (102 MB/rank, rotating RNG)"},
             "roofline": {"bound": "nvlink", "achieved": dev_bytes / (ms * 1e-3) / 1e9,
                          "peak": 770.0, "unit": "GB/s",
-                         "frac": dev_bytes / (ms * 1e-3) / 1e9 / 770.0, "traffic": None,
+                         "frac": dev_bytes / (ms * 1e-3) / 1e9 / 770.0,
+                         "traffic": dev_bytes,
+                         "traffic_note": "bytes each rank sends per step over NVLink (both "
+                                         "exchange rounds, from the piece tables); the kernels' "
+                                         "DRAM traffic is in profiles/round2_launches_sra8_emul.csv",
                          "kernel": "whole SRA step (compressed bytes over NVLink)",
                          "peak_kind": "measured peer copy per direction (B200_PROFILING.md)"},
-            "cpu_baseline": None,
+            "cpu_baseline": cb,
             "e2e": {"value": busbw(e2e_ms), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
                     "d2h_bytes_per_step": 4 * n},
             "gpu_launches": car.launches_per_step() * args.steps,
