@@ -535,6 +535,35 @@ __global__ void __launch_bounds__(32 * kWarps, 1)
 // copied into the message by the warp.  Keys: inline, or span-layout
 // prefixes at run offset p.keys (gcx_plan_keys / gcx_make_key_prefix).
 // ---------------------------------------------------------------------------
+// Raw pieces (CodecMode::uncompressed) travel as f32.  A warp (or CTA) copies
+// or folds a tile of them with 16-byte accesses and 4 loads in flight per
+// lane: a lane-strided scalar loop keeps one dependent load per iteration in
+// flight and made a warp with a 4096-element raw tile the kernel's straggler.
+__device__ __forceinline__ void raw_copy(const float* __restrict__ in, float* __restrict__ out,
+                                         uint32_t count, float div, float recip, bool pow2,
+                                         uint32_t tid, uint32_t nthreads) {
+  if (((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u) == 0) {
+    const uint32_t n4 = count >> 2;
+    const float4* i4 = reinterpret_cast<const float4*>(in);
+    float4* o4 = reinterpret_cast<float4*>(out);
+#pragma unroll 4
+    for (uint32_t k = tid; k < n4; k += nthreads) {
+      float4 v = __ldcs(i4 + k);
+      v.x = apply_divisor(v.x, div, recip, pow2);
+      v.y = apply_divisor(v.y, div, recip, pow2);
+      v.z = apply_divisor(v.z, div, recip, pow2);
+      v.w = apply_divisor(v.w, div, recip, pow2);
+      __stcs(o4 + k, v);
+    }
+    for (uint32_t e = (n4 << 2) + tid; e < count; e += nthreads)
+      out[e] = apply_divisor(__ldcs(in + e), div, recip, pow2);
+  } else {
+#pragma unroll 8
+    for (uint32_t e = tid; e < count; e += nthreads)
+      out[e] = apply_divisor(__ldcs(in + e), div, recip, pow2);
+  }
+}
+
 struct SpanPiecesArgs {
   gcx_plan::PlanView pv;
   uint32_t flags;
@@ -765,6 +794,7 @@ __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A
       const float* xs = A.src + p.src + cur.start;
       float* d = reinterpret_cast<float*>(A.msg + p.norms) + cur.start;
       if (FOLD) {  // the raw fold, ascending id (collectives.cpp:268-279)
+#pragma unroll 4
         for (uint32_t e = lane; e < cur.count; e += 32) {
           float acc = 0.0f;
           for (uint32_t id = 0; id < A.nodes; ++id) {
@@ -778,7 +808,7 @@ __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A
           d[e] = acc;
         }
       } else {
-        for (uint32_t e = lane; e < cur.count; e += 32) d[e] = __ldcs(xs + e);
+        raw_copy(xs, d, cur.count, 1.0f, 1.0f, true, lane, 32);
       }
       if (KM != kKmInline && more && nxt.p.bits > 0) {  // the key ring's next group
         const uint4* kn = key_group(nxt, 0);
@@ -1158,10 +1188,8 @@ __global__ void __launch_bounds__(32 * kDWarps) k_dspan_pieces(gcx_plan::PlanVie
     const gcx_piece& p = c.p;
     switch (p.bits) {
       case 0: {  // raw piece: f32 payload at p.norms, divided (finalize's average)
-        const float* in = reinterpret_cast<const float*>(msg + p.norms) + c.start;
-        float* out = dst + p.src + c.start;
-        for (uint32_t e = lane; e < c.count; e += 32)
-          __stcs(out + e, apply_divisor(__ldcs(in + e), div, recip, pow2));
+        raw_copy(reinterpret_cast<const float*>(msg + p.norms) + c.start, dst + p.src + c.start,
+                 c.count, div, recip, pow2, lane, 32);
         break;
       }
       case 1: dspan_piece_tile<1>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
@@ -1367,9 +1395,12 @@ cudaError_t gcx_span_decode_pieces(const gcx_piece* pieces, const uint32_t* tile
 //   D  the tile's packed words leave with one bulk store.
 // ---------------------------------------------------------------------------
 constexpr int kFoldWarps = 4;
+#ifndef GCX_FOLD_MINB
+#define GCX_FOLD_MINB 3  // resident CTAs per SM (registers <= 168)
+#endif
 
 template <uint32_t BITS, int KM>
-__global__ void __launch_bounds__(32 * kFoldWarps, 1) k_span_fold_cta(SpanPiecesArgs A) {
+__global__ void __launch_bounds__(32 * kFoldWarps, GCX_FOLD_MINB) k_span_fold_cta(SpanPiecesArgs A) {
   constexpr uint32_t W = BITS + 1;
   extern __shared__ __align__(1024) unsigned char span_smem[];
   float* slots = reinterpret_cast<float*>(span_smem);                       // 4 x 4 KB
@@ -1392,6 +1423,7 @@ __global__ void __launch_bounds__(32 * kFoldWarps, 1) k_span_fold_cta(SpanPieces
     if (p.bits == 0) {  // raw piece: the raw fold, ascending id (collectives.cpp:268-279)
       const float* xs = A.src + p.src + cur.start;
       float* d = reinterpret_cast<float*>(A.msg + p.norms) + cur.start;
+#pragma unroll 4
       for (uint32_t e = threadIdx.x; e < cur.count; e += 32 * kFoldWarps) {
         float acc = 0.0f;
         for (uint32_t id = 0; id < A.nodes; ++id) {
