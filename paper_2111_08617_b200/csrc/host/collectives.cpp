@@ -246,6 +246,17 @@ namespace {
 // one seed, its key-table plan), uploaded into one blob.
 struct Table;
 bool onestep_table(const Table& t);
+// Shared key tables (N > 2 stage 1) take the span K1 in key-table mode
+// (default; 4 % faster per rank at N = 8 than the CTA K1 once raw tiles were
+// vectorised); GCX_SPAN_SHARED=0 restores the lane-group layout + CTA K1
+// (measurement switch)
+bool span_shared_tables() {
+  static const bool v = [] {
+    const char* e = std::getenv("GCX_SPAN_SHARED");
+    return e == nullptr || e[0] != '0';
+  }();
+  return v;
+}
 
 struct Table {
   std::vector<gcx_piece> pieces;
@@ -280,12 +291,11 @@ struct Table {
         key_len = std::uint64_t(len);
       };
       plan_keys(GCX_KEYS_AUTO);
-      // The span K1 wins when it hashes straight from the prefixes (one
-      // launch: an unshared, large key table — an owner chunk, N = 2's peer
-      // chunk); tables whose key slots are read by several pieces (N > 2
-      // stage 1) keep the two-step key table + CTA K1, so they take the
-      // lane-group layout and drop GCX_F_SPAN_ENC.
-      if ((flags & GCX_F_SPAN_ENC) && !onestep_table(*this) && !keep_span) {
+      // Span tables keep the span key layout (prefix one-step or key-table
+      // mode of the span K1); with GCX_SPAN_SHARED=0 tables whose key slots
+      // are read by several pieces (N > 2 stage 1) fall back to the two-step
+      // key table + CTA K1, in the lane-group layout without GCX_F_SPAN_ENC.
+      if ((flags & GCX_F_SPAN_ENC) && !onestep_table(*this) && !keep_span && !span_shared_tables()) {
         flags &= ~(GCX_F_SPAN_ENC | (0xFFu << GCX_F_SPAN_BITS_SHIFT));
         plan_keys(GCX_KEYS_LANE_GROUP);
       }
