@@ -1396,7 +1396,7 @@ cudaError_t gcx_span_decode_pieces(const gcx_piece* pieces, const uint32_t* tile
 // ---------------------------------------------------------------------------
 constexpr int kFoldWarps = 4;
 #ifndef GCX_FOLD_MINB
-#define GCX_FOLD_MINB 3  // resident CTAs per SM (registers <= 168)
+#define GCX_FOLD_MINB 4  // resident CTAs per SM (registers <= 128): the owner chunk fits one wave
 #endif
 
 template <uint32_t BITS, int KM>
