@@ -10,7 +10,13 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 400 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 400 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 > /dev/null 2>&1
-timeout 400 ncu --set full --clock-control none --import-source on -k regex:k_span -s 2 -c 1 -o gpurun_out/c1_k_span python bench.py --steps 2 --warmup 3 > /dev/null 2>&1
-timeout 400 ncu --set full --clock-control none --import-source on -k regex:k_dspan -s 2 -c 1 -o gpurun_out/c1_k_dspan python bench.py --steps 2 --warmup 3 > /dev/null 2>&1
+# full captures stay on the box (a K1 .ncu-rep is ~50 MB; gpurun merges <= 64 MiB):
+# their summaries and K1's source page come back
+mkdir -p /tmp/ncu
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:k_span -s 2 -c 1 -o /tmp/ncu/c1_k_span python bench.py --steps 2 --warmup 3 > /dev/null 2>&1
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:k_dspan -s 2 -c 1 -o /tmp/ncu/c1_k_dspan python bench.py --steps 2 --warmup 3 > /dev/null 2>&1
+python scripts/ncu_summary.py /tmp/ncu/c1_k_span.ncu-rep round2_c1_k_span gpurun_out > /dev/null
+python scripts/ncu_summary.py /tmp/ncu/c1_k_dspan.ncu-rep round2_c1_k_dspan gpurun_out > /dev/null
+ncu -i /tmp/ncu/c1_k_span.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > gpurun_out/k_span_source.csv.gz
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/sra8_launches.csv python scripts/sra_emul_profile.py 8 > /dev/null 2>&1
 tail -4 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err; cat gpurun_out/bench_ref.json; ls gpurun_out
