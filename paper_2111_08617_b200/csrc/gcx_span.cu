@@ -64,6 +64,9 @@ constexpr uint32_t kSlotFloats = 32 * 32;
 #define GCX_SPAN_WARPS 4
 #endif
 constexpr int kWarps = GCX_SPAN_WARPS;
+#ifndef GCX_SMALL_TILES_PER_SM
+#define GCX_SMALL_TILES_PER_SM 2  // tables of at most this many tiles per SM: CTA-per-tile kernels
+#endif
 
 // per-warp shared memory: kSlots swizzled quarter slots, the packed output
 // words of one tile (128 groups x W words), kSlots mbarriers; 1 KB aligned
@@ -591,7 +594,8 @@ struct SpanPiecesArgs {
 template <uint32_t BITS>
 __device__ __forceinline__ void fold_tile(const SpanPiecesArgs& A, const gcx_piece& p,
                                           uint32_t start, uint32_t count, float* slots,
-                                          uint32_t lane, uint32_t r0 = 0, uint32_t r1 = 32) {
+                                          uint32_t lane, uint32_t r0 = 0, uint32_t r1 = 32,
+                                          uint32_t rstep = 1) {
   constexpr uint32_t W = BITS + 1, S = (1u << BITS) - 1, F = 2u << BITS;
   const uint32_t f = lane & (F - 1u), level = f & S, sign = f >> BITS;
   const double dl = double(level);
@@ -638,9 +642,15 @@ __device__ __forceinline__ void fold_tile(const SpanPiecesArgs& A, const gcx_pie
   RowLoads cur;
   load_row(r0, cur);
 #pragma unroll 1
-  for (uint32_t r = r0; r < r1; ++r) {
+  for (uint32_t r = r0; r < r1; r += rstep) {
+    if (r * 128u >= count) {  // the rest of this lane set's rows lie past the piece: zeros
+      for (; r < r1; r += rstep)
+        *reinterpret_cast<float4*>(slots + (lane >> 3) * kSlotFloats + r * 32u +
+                                   (((lane & 7u) ^ (r & 7u)) << 2)) = make_float4(0.f, 0.f, 0.f, 0.f);
+      break;
+    }
     RowLoads nxt;
-    if (r + 1 < r1) load_row(r + 1, nxt);
+    if (r + rstep < r1) load_row(r + rstep, nxt);
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (uint32_t id = 0; id < 8; ++id) {
@@ -1105,7 +1115,8 @@ template <uint32_t BITS>
 __device__ __forceinline__ void dspan_piece_tile(const gcx_piece& p, uint32_t start, uint32_t count,
                                                  const uint8_t* __restrict__ msg,
                                                  float* __restrict__ dst, float div, float recip,
-                                                 bool pow2, uint32_t* words, uint32_t lane) {
+                                                 bool pow2, uint32_t* words, uint32_t lane,
+                                                 uint32_t c_lo = 0, uint32_t c_hi = 32) {
   constexpr uint32_t W = BITS + 1, S = (1u << BITS) - 1, F = 2u << BITS;
   constexpr uint32_t TW = 128u * W;
   const uint32_t f = lane & (F - 1u), level = f & S, sign = f >> BITS;
@@ -1122,15 +1133,16 @@ __device__ __forceinline__ void dspan_piece_tile(const gcx_piece& p, uint32_t st
   const uint32_t nreg = lane < (kWTile >> lgb) && b0 + lane < nbk
                             ? __ldg(reinterpret_cast<const uint32_t*>(msg + p.norms) + b0 + lane)
                             : 0u;
-  if (full && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+  if (c_lo == 0 && c_hi == 32 && full && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
     uint4 st[W];
 #pragma unroll
     for (uint32_t k = 0; k < W; ++k) st[k] = __ldcs(reinterpret_cast<const uint4*>(src) + k * 32 + lane);
 #pragma unroll
     for (uint32_t k = 0; k < W; ++k) reinterpret_cast<uint4*>(words)[k * 32 + lane] = st[k];
-  } else {
+  } else {  // the words of chunks [c_lo, c_hi) (a lane's window stays inside its chunk)
     const uint32_t nw = (count * W + 31) / 32;
-    for (uint32_t k = lane; k < TW; k += 32) words[k] = k < nw ? src[k] : 0u;
+    const uint32_t k1 = min(TW, c_hi * 4 * W);
+    for (uint32_t k = c_lo * 4 * W + lane; k < k1; k += 32) words[k] = k < nw ? src[k] : 0u;
   }
   __syncwarp();
   float* out = dst + p.src + start + 4 * lane;
@@ -1139,12 +1151,13 @@ __device__ __forceinline__ void dspan_piece_tile(const gcx_piece& p, uint32_t st
   // entries (one per chunk; chunks of one bucket compute the same entry),
   // then 8 chunks decoded by shuffles
 #pragma unroll 1
-  for (uint32_t bb = 0; bb < 4; ++bb) {
-    if (bb * 1024 >= count) break;
+  for (uint32_t c0 = c_lo; c0 < c_hi; c0 += 8) {
+    if (c0 * 128 >= count) break;
+    const uint32_t bb8 = c0;  // first chunk of the batch
     float entry[8];
 #pragma unroll
     for (uint32_t cc = 0; cc < 8; ++cc) {
-      const uint32_t nu = __shfl_sync(0xffffffffu, nreg, (bb * 8 + cc) >> bshift);
+      const uint32_t nu = __shfl_sync(0xffffffffu, nreg, min(bb8 + cc, 31u) >> bshift);
       const double nl = __dmul_rn(double(__uint_as_float(nu)), dl);  // exact
       const double q0 = __dmul_rn(nl, ys);
       const double q = __fma_rn(__fma_rn(-sd, q0, nl), ys, q0);  // RN(nl / s), see dequant_field
@@ -1153,8 +1166,8 @@ __device__ __forceinline__ void dspan_piece_tile(const gcx_piece& p, uint32_t st
     }
 #pragma unroll
     for (uint32_t cc = 0; cc < 8; ++cc) {
-      const uint32_t c = bb * 8 + cc;
-      if (c * 128 >= count) break;
+      const uint32_t c = bb8 + cc;
+      if (c >= c_hi || c * 128 >= count) break;
       const uint32_t* cw = words + c * 4 * W + qw;
       const uint32_t win = two ? __funnelshift_r(cw[0], cw[1], qsh) : (cw[0] >> qsh);
       float v[4];
@@ -1198,6 +1211,41 @@ __global__ void __launch_bounds__(32 * kDWarps) k_dspan_pieces(gcx_plan::PlanVie
       case 4: dspan_piece_tile<4>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
       default: break;
     }
+  }
+}
+
+// Short tables (a small message): a CTA of 8 warps per tile, warp w decoding
+// chunks 4w..4w+3, so one tile's latency is an eighth of a warp's.
+__global__ void __launch_bounds__(32 * kDWarps) k_dspan_pieces_small(gcx_plan::PlanView pv,
+                                                                     const uint8_t* __restrict__ msg,
+                                                                     float* __restrict__ dst,
+                                                                     float div, float recip,
+                                                                     bool pow2) {
+  __shared__ __align__(16) uint32_t words[128 * 5 + 4];
+  __shared__ gcx_plan::TileCtx ctx_s;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  for (uint32_t t = blockIdx.x; t < pv.ntiles; t += gridDim.x) {
+    if (warp == 0) {
+      gcx_plan::TileCtx c;
+      gcx_plan::locate_warp(pv, t, c);
+      if (lane == 0) ctx_s = c;
+    }
+    __syncthreads();
+    const gcx_plan::TileCtx c = ctx_s;
+    const gcx_piece& p = c.p;
+    const uint32_t c_lo = 4 * warp, c_hi = 4 * warp + 4;
+    switch (p.bits) {
+      case 0:
+        raw_copy(reinterpret_cast<const float*>(msg + p.norms) + c.start, dst + p.src + c.start,
+                 c.count, div, recip, pow2, threadIdx.x, 32 * kDWarps);
+        break;
+      case 1: dspan_piece_tile<1>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane, c_lo, c_hi); break;
+      case 2: dspan_piece_tile<2>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane, c_lo, c_hi); break;
+      case 3: dspan_piece_tile<3>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane, c_lo, c_hi); break;
+      case 4: dspan_piece_tile<4>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane, c_lo, c_hi); break;
+      default: break;
+    }
+    __syncthreads();
   }
 }
 
@@ -1377,6 +1425,11 @@ cudaError_t gcx_span_decode_pieces(const gcx_piece* pieces, const uint32_t* tile
   gcx_plan::PlanView pv{pieces, tile_prefix, npieces, ntiles, {}};
   int e2 = 0;
   const bool pow2 = std::frexp(divisor, &e2) == 0.5f;
+  if (ntiles <= uint32_t(sms) * GCX_SMALL_TILES_PER_SM) {  // short table: CTA per tile
+    k_dspan_pieces_small<<<ntiles, 32 * kDWarps, 0, st>>>(pv, msg, dst, divisor, 1.0f / divisor,
+                                                          pow2);
+    return cudaGetLastError();
+  }
   uint32_t grid = (ntiles + kDWarps - 1) / kDWarps;
   if (grid > uint32_t(sms * occ)) grid = uint32_t(sms * occ);
   if (grid == 0) grid = 1;
@@ -1399,7 +1452,10 @@ constexpr int kFoldWarps = 4;
 #define GCX_FOLD_MINB 4  // resident CTAs per SM (registers <= 128): the owner chunk fits one wave
 #endif
 
-template <uint32_t BITS, int KM>
+// FOLD = false is the same CTA-per-tile K1 fed from `src` (phase A stages
+// rows 8w..8w+7 by coalesced loads): the small-message form of k_span_pieces,
+// whose one-warp tiles leave a short table latency-bound (bucket 128 only).
+template <uint32_t BITS, int KM, bool FOLD>
 __global__ void __launch_bounds__(32 * kFoldWarps, GCX_FOLD_MINB) k_span_fold_cta(SpanPiecesArgs A) {
   constexpr uint32_t W = BITS + 1;
   extern __shared__ __align__(1024) unsigned char span_smem[];
@@ -1410,7 +1466,6 @@ __global__ void __launch_bounds__(32 * kFoldWarps, GCX_FOLD_MINB) k_span_fold_ct
   __shared__ gcx_plan::TileCtx ctx_s;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const HashK shk = make_hashk();
-  const uint32_t s_lo = uint32_t(A.seed), s_hi = uint32_t(A.seed >> 32);
   for (uint32_t t = blockIdx.x; t < A.pv.ntiles; t += gridDim.x) {
     if (warp == 0) {
       gcx_plan::TileCtx c;
@@ -1420,6 +1475,12 @@ __global__ void __launch_bounds__(32 * kFoldWarps, GCX_FOLD_MINB) k_span_fold_ct
     __syncthreads();
     const gcx_plan::TileCtx cur = ctx_s;
     const gcx_piece& p = cur.p;
+    if (p.bits == 0 && !FOLD) {  // raw piece: its f32 values are the payload
+      raw_copy(A.src + p.src + cur.start, reinterpret_cast<float*>(A.msg + p.norms) + cur.start,
+               cur.count, 1.0f, 1.0f, true, threadIdx.x, 32 * kFoldWarps);
+      __syncthreads();
+      continue;
+    }
     if (p.bits == 0) {  // raw piece: the raw fold, ascending id (collectives.cpp:268-279)
       const float* xs = A.src + p.src + cur.start;
       float* d = reinterpret_cast<float*>(A.msg + p.norms) + cur.start;
@@ -1439,8 +1500,31 @@ __global__ void __launch_bounds__(32 * kFoldWarps, GCX_FOLD_MINB) k_span_fold_ct
       __syncthreads();
       continue;
     }
-    // A: fold
-    fold_tile<BITS>(A, p, cur.start, cur.count, slots, lane, 8 * warp, 8 * warp + 8);
+    const uint64_t seed = (A.flags & GCX_F_PIECE_SEEDS) ? p.seed : A.seed;
+    const uint32_t s_lo = uint32_t(seed), s_hi = uint32_t(seed >> 32);
+    // A: fold (or stage) rows 8w..8w+7
+    if constexpr (FOLD) {
+      // rows warp, warp+4, ...: a short tile's rows spread over all four warps
+      fold_tile<BITS>(A, p, cur.start, cur.count, slots, lane, warp, 32, kFoldWarps);
+    } else {
+      const float* xs = A.src + p.src + cur.start;
+      const bool al = (reinterpret_cast<uintptr_t>(A.src + p.src) & 15u) == 0;
+#pragma unroll
+      for (uint32_t r = warp; r < 32; r += kFoldWarps) {  // rows spread over the warps
+        const uint32_t e = r * 128u + 4 * lane;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (e + 4 <= cur.count && al) {
+          v = __ldcs(reinterpret_cast<const float4*>(xs + e));
+        } else {
+          if (e < cur.count) v.x = xs[e];
+          if (e + 1 < cur.count) v.y = xs[e + 1];
+          if (e + 2 < cur.count) v.z = xs[e + 2];
+          if (e + 3 < cur.count) v.w = xs[e + 3];
+        }
+        *reinterpret_cast<float4*>(slots + (lane >> 3) * kSlotFloats + r * 32u +
+                                   (((lane & 7u) ^ (r & 7u)) << 2)) = v;
+      }
+    }
     __syncthreads();
     RowView rv;
 #pragma unroll
@@ -1512,7 +1596,7 @@ __global__ void __launch_bounds__(32 * kFoldWarps, GCX_FOLD_MINB) k_span_fold_ct
         for (int m = 0; m < int(W); ++m) wout[m] = w[m];
       } else {
         span_group_exact<BITS, 7, KM>(
-            rv, g, i0, nug, A.seed,
+            rv, g, i0, nug, seed,
             KM != kKmInline ? A.keys + ((p.keys + cur.start) >> 12) * 8192u : nullptr, lane, wout);
       }
     }
@@ -1550,10 +1634,10 @@ SpanPiecesFn pick_pieces_km(int km) {
 static SpanPiecesFn pick_fold(int bits, bool prefix) {
   if (GCX_FOLD_CTA) {
     switch (bits) {
-      case 1: return prefix ? k_span_fold_cta<1, kKmPrefix> : k_span_fold_cta<1, kKmInline>;
-      case 2: return prefix ? k_span_fold_cta<2, kKmPrefix> : k_span_fold_cta<2, kKmInline>;
-      case 3: return prefix ? k_span_fold_cta<3, kKmPrefix> : k_span_fold_cta<3, kKmInline>;
-      case 4: return prefix ? k_span_fold_cta<4, kKmPrefix> : k_span_fold_cta<4, kKmInline>;
+      case 1: return prefix ? k_span_fold_cta<1, kKmPrefix, true> : k_span_fold_cta<1, kKmInline, true>;
+      case 2: return prefix ? k_span_fold_cta<2, kKmPrefix, true> : k_span_fold_cta<2, kKmInline, true>;
+      case 3: return prefix ? k_span_fold_cta<3, kKmPrefix, true> : k_span_fold_cta<3, kKmInline, true>;
+      case 4: return prefix ? k_span_fold_cta<4, kKmPrefix, true> : k_span_fold_cta<4, kKmInline, true>;
       default: return nullptr;
     }
   }
@@ -1590,6 +1674,64 @@ static SpanPiecesFn pick_pieces(int bits, int lgb, int km) {
   }
 }
 
+
+template <uint32_t BITS>
+static SpanPiecesFn pick_small_km(int km) {
+  switch (km) {
+    case kKmTable: return k_span_fold_cta<BITS, kKmTable, false>;
+    case kKmPrefix: return k_span_fold_cta<BITS, kKmPrefix, false>;
+    default: return k_span_fold_cta<BITS, kKmInline, false>;
+  }
+}
+
+static SpanPiecesFn pick_small(int bits, int km) {
+  switch (bits) {
+    case 1: return pick_small_km<1>(km);
+    case 2: return pick_small_km<2>(km);
+    case 3: return pick_small_km<3>(km);
+    case 4: return pick_small_km<4>(km);
+    case 5: return pick_small_km<5>(km);
+    case 6: return pick_small_km<6>(km);
+    case 7: return pick_small_km<7>(km);
+    case 8: return pick_small_km<8>(km);
+    default: return nullptr;
+  }
+}
+
+// K1 for short tables (a small message's chunks): a CTA of 4 warps per tile
+static cudaError_t span_small_encode(const gcx_piece* pieces, const uint32_t* tile_prefix,
+                                     uint32_t npieces, uint32_t ntiles, uint32_t flags,
+                                     uint64_t seed, const float* src, uint8_t* msg,
+                                     const unsigned long long* keys, unsigned long long* bad,
+                                     int bits, int km, int sms, cudaStream_t st) {
+  SpanPiecesFn fn = pick_small(bits, km);
+  if (fn == nullptr) return cudaErrorInvalidValue;
+  const uint32_t W = uint32_t(bits) + 1;
+  const size_t smem = size_t(4 * kSlotFloats * 4 + out_words(W) * 4 + 64 * 4);
+  static thread_local bool cfg[9][3] = {};
+  if (!cfg[bits][km]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    cfg[bits][km] = true;
+  }
+  SpanPiecesArgs a;
+  a.pv = gcx_plan::PlanView{pieces, tile_prefix, npieces, ntiles, {}};
+  a.flags = flags;
+  a.seed = seed;
+  a.src = src;
+  a.msg = msg;
+  a.keys = reinterpret_cast<const uint32_t*>(keys);
+  a.bad = bad;
+  a.recv = nullptr;
+  a.slot_stride = 0;
+  a.nodes = 0;
+  a.me = 0;
+  uint32_t grid = ntiles;
+  if (grid > uint32_t(sms * GCX_FOLD_MINB)) grid = uint32_t(sms * GCX_FOLD_MINB);
+  fn<<<grid > 0 ? grid : 1, 32 * kFoldWarps, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t gcx_span_encode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix,
                                    uint32_t npieces, uint32_t ntiles, uint32_t flags, uint64_t seed,
                                    const float* src, uint8_t* msg, const unsigned long long* keys,
@@ -1597,6 +1739,9 @@ cudaError_t gcx_span_encode_pieces(const gcx_piece* pieces, const uint32_t* tile
   const int bits = int((flags >> GCX_F_SPAN_BITS_SHIFT) & 15u);
   const int lgb = int((flags >> GCX_F_SPAN_LGB_SHIFT) & 15u);
   const int km = keys == nullptr ? kKmInline : (flags & GCX_F_KEY_PREFIX) ? kKmPrefix : kKmTable;
+  if (lgb == 7 && ntiles <= uint32_t(sms) * GCX_SMALL_TILES_PER_SM)
+    return span_small_encode(pieces, tile_prefix, npieces, ntiles, flags, seed, src, msg, keys, bad,
+                             bits, km, sms, st);
   SpanPiecesFn fn = pick_pieces(bits, lgb, km);
   if (fn == nullptr) return cudaErrorInvalidValue;
   const size_t smem = size_t(kWarps) * warp_smem_bytes(uint32_t(bits) + 1);
