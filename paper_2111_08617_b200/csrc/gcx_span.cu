@@ -140,6 +140,7 @@ SpanFn pick_lgb(int lgb, bool prefix) {
     case 5: return prefix ? k_span<BITS, 5, true> : k_span<BITS, 5, false>;
     case 6: return prefix ? k_span<BITS, 6, true> : k_span<BITS, 6, false>;
     case 7: return prefix ? k_span<BITS, 7, true> : k_span<BITS, 7, false>;
+    case 9: return prefix ? k_span<BITS, 9, true> : k_span<BITS, 9, false>;
     default: return nullptr;
   }
 }
@@ -159,7 +160,7 @@ SpanFn pick(int bits, int lgb, bool prefix) {
 }
 
 int lgb_of(uint64_t bucket) {
-  return bucket == 32 ? 5 : bucket == 64 ? 6 : bucket == 128 ? 7 : -1;
+  return bucket == 32 ? 5 : bucket == 64 ? 6 : bucket == 128 ? 7 : bucket == 512 ? 9 : -1;
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)

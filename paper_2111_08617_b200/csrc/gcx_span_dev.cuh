@@ -264,6 +264,65 @@ static __device__ __noinline__ uint32_t span_norm_exact(RowView rv, uint32_t e0,
   return __float_as_uint(__double2float_rn(__dsqrt_rn(sq)));
 }
 
+// Pass 1 for buckets of 2^LGB > 128 elements (RPB = 2^(LGB-7) consecutive
+// rows per bucket): the bucket's first lane runs the reference's sequential
+// FP64 chain over its RPB rows (codec.cpp:41-48) and every lane gets its
+// row's bucket norm by shuffle.  first_bad (lead lanes): the bucket-relative
+// index of the first non-finite input, or ~0.
+template <int LGB>
+__device__ __forceinline__ void span_pass1_big(const RowView& rv, uint32_t lane, uint32_t& nu,
+                                               bool& careful, uint32_t& first_bad) {
+  constexpr uint32_t RPB = 1u << (LGB - 7);
+  const bool lead = (lane & (RPB - 1u)) == 0;
+  double sq = 0.0;
+  first_bad = ~0u;
+  if (lead) {
+#pragma unroll 1
+    for (uint32_t k = 0; k < RPB; ++k) {
+      const uint32_t row = lane + k;
+#pragma unroll
+      for (uint32_t g = 0; g < 4; ++g) {
+        const float* rp = rv.slot[g] + row * 32u;
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q) {
+          const float4 v = *reinterpret_cast<const float4*>(rp + ((q ^ (row & 7u)) << 2));
+          double d = double(v.x);
+          sq = __fma_rn(d, d, sq);
+          d = double(v.y);
+          sq = __fma_rn(d, d, sq);
+          d = double(v.z);
+          sq = __fma_rn(d, d, sq);
+          d = double(v.w);
+          sq = __fma_rn(d, d, sq);
+        }
+      }
+    }
+  }
+  const bool c = lead && (uint32_t(__double2hiint(sq)) & 0x7FF00000u) == 0x7FF00000u;
+  uint32_t v = 0u;
+  if (lead) {
+    if (c) {  // exact sums and the first non-finite input, row by row
+      double sx = 0.0;
+      for (uint32_t k = 0; k < RPB; ++k) {
+        RowView rk = rv;
+        rk.r = lane + k;
+        for (uint32_t e = 0; e < kSpan; ++e) {
+          const uint32_t ua = __float_as_uint(rk.at(e)) & 0x7FFFFFFFu;
+          if (ua >= 0x7F800000u && first_bad == ~0u) first_bad = k * kSpan + e;
+          const double d = f32abs_to_f64_nb(ua);
+          sx = __fma_rn(d, d, sx);
+        }
+      }
+      v = __float_as_uint(__double2float_rn(__dsqrt_rn(sx)));
+    } else {
+      v = __float_as_uint(__double2float_rn(__dsqrt_rn(sq)));
+    }
+  }
+  const uint32_t src = lane & ~(RPB - 1u);
+  nu = __shfl_sync(0xffffffffu, v, src);
+  careful = __shfl_sync(0xffffffffu, c ? 1u : 0u, src) != 0u;
+}
+
 struct SpanArgs {
   const float* x;
   uint32_t n;
@@ -357,9 +416,9 @@ template <uint32_t BITS, int LGB, bool PREFIX>
 __global__ void __launch_bounds__(32 * kWarps, 1)
     k_span(const __grid_constant__ CUtensorMap tmap, SpanArgs A) {
   constexpr uint32_t W = BITS + 1;
-  constexpr uint32_t BL = 1u << LGB;  // bucket length
-  constexpr uint32_t NB = kSpan / BL;  // buckets per row (1, 2, 4)
-  constexpr uint32_t GPB = BL / 32;    // groups per bucket (4, 2, 1)
+  constexpr uint32_t BL = 1u << LGB;                         // bucket length
+  constexpr uint32_t NB = BL <= kSpan ? kSpan / BL : 1u;      // buckets per row (1, 2, 4)
+  constexpr uint32_t GPB = BL <= kSpan ? BL / 32 : 4u;        // groups per bucket in a row
   extern __shared__ __align__(1024) unsigned char span_smem[];
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   unsigned char* base = span_smem + warp * warp_smem_bytes(W);
@@ -426,7 +485,16 @@ __global__ void __launch_bounds__(32 * kWarps, 1)
     // ---- pass 1: sequential FP64 norms of the row's buckets, quarter by quarter ----
     uint32_t nu[NB];
     bool careful[NB];
-    {
+    if constexpr (BL > kSpan) {  // a bucket spans rows: its first lane sums them
+#pragma unroll
+      for (uint32_t g = 0; g < 4; ++g) wait_q(4 * j + g);
+      uint32_t fb;
+      span_pass1_big<LGB>(rv, lane, nu[0], careful[0], fb);
+      if ((lane & (BL / kSpan - 1u)) == 0) {
+        if (fb != ~0u && A.bad != nullptr) atomicMin(A.bad, (unsigned long long)(i_lane + fb));
+        if (full || i_lane < A.n) A.norms[i_lane >> LGB] = __uint_as_float(nu[0]);
+      }
+    } else {
       double sq = 0.0;
 #pragma unroll
       for (uint32_t g = 0; g < 4; ++g) {
@@ -593,7 +661,7 @@ struct SpanPiecesArgs {
 // slot l/8, where the span K1 passes read it.  Row r+1's loads (the peers'
 // norms and packed windows, the owner's raw quad) are issued before row r is
 // folded.  Requires bits <= 4 and bucket 128; nodes <= 8.
-template <uint32_t BITS>
+template <uint32_t BITS, int LGB>
 __device__ __forceinline__ void fold_tile(const SpanPiecesArgs& A, const gcx_piece& p,
                                           uint32_t start, uint32_t count, float* slots,
                                           uint32_t lane, uint32_t r0 = 0, uint32_t r1 = 32,
@@ -632,7 +700,7 @@ __device__ __forceinline__ void fold_tile(const SpanPiecesArgs& A, const gcx_pie
       L.w1[id] = 0u;
       if (id < nodes && id != me && vr > 0) {
         const uint8_t* m = A.recv + uint64_t(id < me ? id : id - 1) * A.slot_stride;
-        L.nu[id] = __ldg(reinterpret_cast<const uint32_t*>(m + p.norms) + (e_row >> 7));
+        L.nu[id] = __ldg(reinterpret_cast<const uint32_t*>(m + p.norms) + (e_row >> LGB));
         if (quad) {
           const uint32_t* wp = reinterpret_cast<const uint32_t*>(m + p.packed) + (e_row >> 5) * W + qw;
           L.w0[id] = __ldg(wp);
@@ -704,11 +772,11 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
 
 template <uint32_t BITS, int LGB, int KM, bool FOLD>
 __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A) {
-  static_assert(!FOLD || (BITS <= 4 && LGB == 7), "the fused fold needs bits <= 4 and bucket 128");
+  static_assert(!FOLD || (BITS <= 4 && LGB >= 7), "the fused fold needs bits <= 4 and bucket >= 128");
   constexpr uint32_t W = BITS + 1;
   constexpr uint32_t BL = 1u << LGB;
-  constexpr uint32_t NB = kSpan / BL;
-  constexpr uint32_t GPB = BL / 32;
+  constexpr uint32_t NB = BL <= kSpan ? kSpan / BL : 1u;
+  constexpr uint32_t GPB = BL <= kSpan ? BL / 32 : 4u;
   extern __shared__ __align__(1024) unsigned char span_smem[];
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   unsigned char* base = span_smem + warp * warp_smem_bytes(W);
@@ -849,14 +917,25 @@ __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A
     for (uint32_t g = 0; g < 4; ++g) rv.slot[g] = slots + (FOLD ? g : (4 * j + g) % kSlots) * kSlotFloats;
     rv.r = lane;
     if (FOLD) {
-      if constexpr (FOLD) fold_tile<BITS>(A, p, cur.start, cur.count, slots, lane);
+      if constexpr (FOLD) fold_tile<BITS, LGB>(A, p, cur.start, cur.count, slots, lane);
       __syncwarp();
     }
 
     // ---- pass 1 ----
     uint32_t nu[NB];
     bool careful[NB];
-    {
+    if constexpr (BL > kSpan) {  // a bucket spans rows: its first lane sums them
+      if (!FOLD) {
+#pragma unroll
+        for (uint32_t g = 0; g < 4; ++g) wait_q(4 * j + g);
+      }
+      uint32_t fb;
+      span_pass1_big<LGB>(rv, lane, nu[0], careful[0], fb);
+      if ((lane & (BL / kSpan - 1u)) == 0) {
+        if (fb != ~0u && A.bad != nullptr) atomicMin(A.bad, pkey | (i_lane + fb));
+        if (i_lane < p.len) norms[i_lane >> LGB] = nu[0];
+      }
+    } else {
       double sq = 0.0;
 #pragma unroll
       for (uint32_t g = 0; g < 4; ++g) {
@@ -1190,7 +1269,7 @@ constexpr int kFoldWarps = 4;
 // FOLD = false is the same CTA-per-tile K1 fed from `src` (phase A stages
 // rows 8w..8w+7 by coalesced loads): the small-message form of k_span_pieces,
 // whose one-warp tiles leave a short table latency-bound (bucket 128 only).
-template <uint32_t BITS, int KM, bool FOLD>
+template <uint32_t BITS, int LGB, int KM, bool FOLD>
 __global__ void __launch_bounds__(32 * kFoldWarps, GCX_FOLD_MINB) k_span_fold_cta(SpanPiecesArgs A) {
   constexpr uint32_t W = BITS + 1;
   extern __shared__ __align__(1024) unsigned char span_smem[];
@@ -1240,7 +1319,7 @@ __global__ void __launch_bounds__(32 * kFoldWarps, GCX_FOLD_MINB) k_span_fold_ct
     // A: fold (or stage) rows 8w..8w+7
     if constexpr (FOLD) {
       // rows warp, warp+4, ...: a short tile's rows spread over all four warps
-      fold_tile<BITS>(A, p, cur.start, cur.count, slots, lane, warp, 32, kFoldWarps);
+      fold_tile<BITS, LGB>(A, p, cur.start, cur.count, slots, lane, warp, 32, kFoldWarps);
     } else {
       const float* xs = A.src + p.src + cur.start;
       const bool al = (reinterpret_cast<uintptr_t>(A.src + p.src) & 15u) == 0;
@@ -1279,39 +1358,50 @@ __global__ void __launch_bounds__(32 * kFoldWarps, GCX_FOLD_MINB) k_span_fold_ct
       }
     }
     if (warp == 0) {
-      double sq = 0.0;
-#pragma unroll
-      for (uint32_t g = 0; g < 4; ++g) {
-        const float* row = rv.slot[g] + lane * 32u;
-#pragma unroll
-        for (uint32_t q = 0; q < 8; ++q) {
-          const float4 v = *reinterpret_cast<const float4*>(row + ((q ^ (lane & 7u)) << 2));
-          double d = double(v.x);
-          sq = __fma_rn(d, d, sq);
-          d = double(v.y);
-          sq = __fma_rn(d, d, sq);
-          d = double(v.z);
-          sq = __fma_rn(d, d, sq);
-          d = double(v.w);
-          sq = __fma_rn(d, d, sq);
-        }
-      }
-      const bool c = (uint32_t(__double2hiint(sq)) & 0x7FF00000u) == 0x7FF00000u;
       uint32_t v;
-      if (c) {
-        v = span_norm_exact(rv, 0, 128, 0u, nullptr);
-        if (A.bad != nullptr)
-          for (uint32_t e = 0; e < 128; ++e)
-            if ((__float_as_uint(rv.at(e)) & 0x7FFFFFFFu) >= 0x7F800000u) {
-              atomicMin(A.bad, (uint64_t(cur.pidx) << 40) | (i_lane + e));
-              break;
-            }
+      bool c;
+      if constexpr (LGB > 7) {  // a bucket spans rows: its first lane sums them
+        uint32_t fb;
+        span_pass1_big<LGB>(rv, lane, v, c, fb);
+        if ((lane & ((1u << (LGB - 7)) - 1u)) == 0) {
+          if (fb != ~0u && A.bad != nullptr)
+            atomicMin(A.bad, (uint64_t(cur.pidx) << 40) | (i_lane + fb));
+          if (i_lane < p.len) reinterpret_cast<uint32_t*>(A.msg + p.norms)[i_lane >> LGB] = v;
+        }
       } else {
-        v = __float_as_uint(__double2float_rn(__dsqrt_rn(sq)));
+        double sq = 0.0;
+#pragma unroll
+        for (uint32_t g = 0; g < 4; ++g) {
+          const float* row = rv.slot[g] + lane * 32u;
+#pragma unroll
+          for (uint32_t q = 0; q < 8; ++q) {
+            const float4 x = *reinterpret_cast<const float4*>(row + ((q ^ (lane & 7u)) << 2));
+            double d = double(x.x);
+            sq = __fma_rn(d, d, sq);
+            d = double(x.y);
+            sq = __fma_rn(d, d, sq);
+            d = double(x.z);
+            sq = __fma_rn(d, d, sq);
+            d = double(x.w);
+            sq = __fma_rn(d, d, sq);
+          }
+        }
+        c = (uint32_t(__double2hiint(sq)) & 0x7FF00000u) == 0x7FF00000u;
+        if (c) {
+          v = span_norm_exact(rv, 0, 128, 0u, nullptr);
+          if (A.bad != nullptr)
+            for (uint32_t e = 0; e < 128; ++e)
+              if ((__float_as_uint(rv.at(e)) & 0x7FFFFFFFu) >= 0x7F800000u) {
+                atomicMin(A.bad, (uint64_t(cur.pidx) << 40) | (i_lane + e));
+                break;
+              }
+        } else {
+          v = __float_as_uint(__double2float_rn(__dsqrt_rn(sq)));
+        }
+        if (i_lane < p.len) reinterpret_cast<uint32_t*>(A.msg + p.norms)[i_lane >> 7] = v;
       }
       nus[lane] = v;
       cars[lane] = c ? 1u : 0u;
-      if (i_lane < p.len) reinterpret_cast<uint32_t*>(A.msg + p.norms)[i_lane >> 7] = v;
       if (lane == 0) bulk_wait_read0();  // the previous tile's bulk store has read outw
     }
     __syncthreads();
@@ -1323,14 +1413,14 @@ __global__ void __launch_bounds__(32 * kFoldWarps, GCX_FOLD_MINB) k_span_fold_ct
       const uint32_t i0 = i_lane + g * 32;
       uint32_t* wout = outw + (lane * 4 + g) * W;
       uint32_t w[W];
-      const bool ok = span_group_fast<BITS, 7, KM>(rv.slot[g], lane, i0, nug, s_lo, s_hi, shk, w, kh,
+      const bool ok = span_group_fast<BITS, LGB, KM>(rv.slot[g], lane, i0, nug, s_lo, s_hi, shk, w, kh,
                                                    kl, nullptr) &&
                       nug != 0u && !car;
       if (ok) {
 #pragma unroll
         for (int m = 0; m < int(W); ++m) wout[m] = w[m];
       } else {
-        span_group_exact<BITS, 7, KM>(
+        span_group_exact<BITS, LGB, KM>(
             rv, g, i0, nug, seed,
             KM != kKmInline ? A.keys + ((p.keys + cur.start) >> 12) * 8192u : nullptr, lane, wout);
       }

@@ -24,21 +24,30 @@ SpanPiecesFn pick_pieces_km(int km) {
 #ifndef GCX_FOLD_CTA
 #define GCX_FOLD_CTA 1  // the fused owner step: 1 = CTA per tile, 0 = warp per tile
 #endif
-static SpanPiecesFn pick_fold(int bits, bool prefix) {
+template <int LGB>
+static SpanPiecesFn pick_fold_lgb(int bits, bool prefix) {
   if (GCX_FOLD_CTA) {
     switch (bits) {
-      case 1: return prefix ? k_span_fold_cta<1, kKmPrefix, true> : k_span_fold_cta<1, kKmInline, true>;
-      case 2: return prefix ? k_span_fold_cta<2, kKmPrefix, true> : k_span_fold_cta<2, kKmInline, true>;
-      case 3: return prefix ? k_span_fold_cta<3, kKmPrefix, true> : k_span_fold_cta<3, kKmInline, true>;
-      case 4: return prefix ? k_span_fold_cta<4, kKmPrefix, true> : k_span_fold_cta<4, kKmInline, true>;
+      case 1: return prefix ? k_span_fold_cta<1, LGB, kKmPrefix, true> : k_span_fold_cta<1, LGB, kKmInline, true>;
+      case 2: return prefix ? k_span_fold_cta<2, LGB, kKmPrefix, true> : k_span_fold_cta<2, LGB, kKmInline, true>;
+      case 3: return prefix ? k_span_fold_cta<3, LGB, kKmPrefix, true> : k_span_fold_cta<3, LGB, kKmInline, true>;
+      case 4: return prefix ? k_span_fold_cta<4, LGB, kKmPrefix, true> : k_span_fold_cta<4, LGB, kKmInline, true>;
       default: return nullptr;
     }
   }
   switch (bits) {
-    case 1: return prefix ? k_span_pieces<1, 7, kKmPrefix, true> : k_span_pieces<1, 7, kKmInline, true>;
-    case 2: return prefix ? k_span_pieces<2, 7, kKmPrefix, true> : k_span_pieces<2, 7, kKmInline, true>;
-    case 3: return prefix ? k_span_pieces<3, 7, kKmPrefix, true> : k_span_pieces<3, 7, kKmInline, true>;
-    case 4: return prefix ? k_span_pieces<4, 7, kKmPrefix, true> : k_span_pieces<4, 7, kKmInline, true>;
+    case 1: return prefix ? k_span_pieces<1, LGB, kKmPrefix, true> : k_span_pieces<1, LGB, kKmInline, true>;
+    case 2: return prefix ? k_span_pieces<2, LGB, kKmPrefix, true> : k_span_pieces<2, LGB, kKmInline, true>;
+    case 3: return prefix ? k_span_pieces<3, LGB, kKmPrefix, true> : k_span_pieces<3, LGB, kKmInline, true>;
+    case 4: return prefix ? k_span_pieces<4, LGB, kKmPrefix, true> : k_span_pieces<4, LGB, kKmInline, true>;
+    default: return nullptr;
+  }
+}
+
+static SpanPiecesFn pick_fold(int bits, int lgb, bool prefix) {
+  switch (lgb) {
+    case 7: return pick_fold_lgb<7>(bits, prefix);
+    case 9: return pick_fold_lgb<9>(bits, prefix);
     default: return nullptr;
   }
 }
@@ -49,6 +58,7 @@ SpanPiecesFn pick_pieces_lgb(int lgb, int km) {
     case 5: return pick_pieces_km<BITS, 5>(km);
     case 6: return pick_pieces_km<BITS, 6>(km);
     case 7: return pick_pieces_km<BITS, 7>(km);
+    case 9: return pick_pieces_km<BITS, 9>(km);
     default: return nullptr;
   }
 }
@@ -68,25 +78,34 @@ static SpanPiecesFn pick_pieces(int bits, int lgb, int km) {
 }
 
 
-template <uint32_t BITS>
+template <uint32_t BITS, int LGB>
 static SpanPiecesFn pick_small_km(int km) {
   switch (km) {
-    case kKmTable: return k_span_fold_cta<BITS, kKmTable, false>;
-    case kKmPrefix: return k_span_fold_cta<BITS, kKmPrefix, false>;
-    default: return k_span_fold_cta<BITS, kKmInline, false>;
+    case kKmTable: return k_span_fold_cta<BITS, LGB, kKmTable, false>;
+    case kKmPrefix: return k_span_fold_cta<BITS, LGB, kKmPrefix, false>;
+    default: return k_span_fold_cta<BITS, LGB, kKmInline, false>;
   }
 }
 
-static SpanPiecesFn pick_small(int bits, int km) {
+template <int LGB>
+static SpanPiecesFn pick_small_lgb(int bits, int km) {
   switch (bits) {
-    case 1: return pick_small_km<1>(km);
-    case 2: return pick_small_km<2>(km);
-    case 3: return pick_small_km<3>(km);
-    case 4: return pick_small_km<4>(km);
-    case 5: return pick_small_km<5>(km);
-    case 6: return pick_small_km<6>(km);
-    case 7: return pick_small_km<7>(km);
-    case 8: return pick_small_km<8>(km);
+    case 1: return pick_small_km<1, LGB>(km);
+    case 2: return pick_small_km<2, LGB>(km);
+    case 3: return pick_small_km<3, LGB>(km);
+    case 4: return pick_small_km<4, LGB>(km);
+    case 5: return pick_small_km<5, LGB>(km);
+    case 6: return pick_small_km<6, LGB>(km);
+    case 7: return pick_small_km<7, LGB>(km);
+    case 8: return pick_small_km<8, LGB>(km);
+    default: return nullptr;
+  }
+}
+
+static SpanPiecesFn pick_small(int bits, int lgb, int km) {
+  switch (lgb) {
+    case 7: return pick_small_lgb<7>(bits, km);
+    case 9: return pick_small_lgb<9>(bits, km);
     default: return nullptr;
   }
 }
@@ -96,16 +115,16 @@ static cudaError_t span_small_encode(const gcx_piece* pieces, const uint32_t* ti
                                      uint32_t npieces, uint32_t ntiles, uint32_t flags,
                                      uint64_t seed, const float* src, uint8_t* msg,
                                      const unsigned long long* keys, unsigned long long* bad,
-                                     int bits, int km, int sms, cudaStream_t st) {
-  SpanPiecesFn fn = pick_small(bits, km);
+                                     int bits, int lgb, int km, int sms, cudaStream_t st) {
+  SpanPiecesFn fn = pick_small(bits, lgb, km);
   if (fn == nullptr) return cudaErrorInvalidValue;
   const uint32_t W = uint32_t(bits) + 1;
   const size_t smem = size_t(4 * kSlotFloats * 4 + out_words(W) * 4 + 64 * 4);
-  static thread_local bool cfg[9][3] = {};
-  if (!cfg[bits][km]) {
+  static thread_local bool cfg[9][13][3] = {};
+  if (!cfg[bits][lgb][km]) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    cfg[bits][km] = true;
+    cfg[bits][lgb][km] = true;
   }
   SpanPiecesArgs a;
   a.pv = gcx_plan::PlanView{pieces, tile_prefix, npieces, ntiles, {}};
@@ -132,9 +151,9 @@ cudaError_t gcx_span_encode_pieces(const gcx_piece* pieces, const uint32_t* tile
   const int bits = int((flags >> GCX_F_SPAN_BITS_SHIFT) & 15u);
   const int lgb = int((flags >> GCX_F_SPAN_LGB_SHIFT) & 15u);
   const int km = keys == nullptr ? kKmInline : (flags & GCX_F_KEY_PREFIX) ? kKmPrefix : kKmTable;
-  if (lgb == 7 && ntiles <= uint32_t(sms) * GCX_SMALL_TILES_PER_SM)
+  if ((lgb == 7 || lgb == 9) && ntiles <= uint32_t(sms) * GCX_SMALL_TILES_PER_SM)
     return span_small_encode(pieces, tile_prefix, npieces, ntiles, flags, seed, src, msg, keys, bad,
-                             bits, km, sms, st);
+                             bits, lgb, km, sms, st);
   SpanPiecesFn fn = pick_pieces(bits, lgb, km);
   if (fn == nullptr) return cudaErrorInvalidValue;
   const size_t smem = size_t(kWarps) * warp_smem_bytes(uint32_t(bits) + 1);
@@ -169,7 +188,8 @@ cudaError_t gcx_span_encode_pieces(const gcx_piece* pieces, const uint32_t* tile
 bool gcx_span_fold_ok(uint32_t flags, uint32_t nodes) {
   const uint32_t bits = (flags >> GCX_F_SPAN_BITS_SHIFT) & 15u;
   const uint32_t lgb = (flags >> GCX_F_SPAN_LGB_SHIFT) & 15u;
-  return (flags & GCX_F_SPAN_ENC) && bits >= 1 && bits <= 4 && lgb == 7 && nodes >= 2 && nodes <= 8;
+  return (flags & GCX_F_SPAN_ENC) && bits >= 1 && bits <= 4 && (lgb == 7 || lgb == 9) && nodes >= 2 &&
+         nodes <= 8;
 }
 
 cudaError_t gcx_span_fold_encode(const gcx_piece* pieces, const uint32_t* tile_prefix,
@@ -180,14 +200,15 @@ cudaError_t gcx_span_fold_encode(const gcx_piece* pieces, const uint32_t* tile_p
                                  cudaStream_t st) {
   if (!gcx_span_fold_ok(flags, nodes) || me >= nodes) return cudaErrorInvalidValue;
   const int bits = int((flags >> GCX_F_SPAN_BITS_SHIFT) & 15u);
-  SpanPiecesFn fn = pick_fold(bits, prefix != nullptr);
+  const int lgb = int((flags >> GCX_F_SPAN_LGB_SHIFT) & 15u);
+  SpanPiecesFn fn = pick_fold(bits, lgb, prefix != nullptr);
   if (fn == nullptr) return cudaErrorInvalidValue;
   const uint32_t W = uint32_t(bits) + 1;
   const size_t smem = GCX_FOLD_CTA ? size_t(4 * kSlotFloats * 4 + out_words(W) * 4 + 64 * 4)
                                    : size_t(kWarps) * warp_smem_bytes(W);
   const int threads = GCX_FOLD_CTA ? 32 * kFoldWarps : 32 * kWarps;
-  static thread_local int occ[9][2] = {};
-  int& o = occ[bits][prefix != nullptr];
+  static thread_local int occ[9][13][2] = {};
+  int& o = occ[bits][lgb][prefix != nullptr];
   if (o == 0) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;

@@ -1,7 +1,7 @@
 """Span K1 (gcx_span.cu: warp tile of 4096, lane span of 128, TMA-staged rows,
 bulk-stored packed words) against the oracle, bit for bit, on the edges the
 kernel has: full tiles + ragged tail, n < one tile, exact multiples of a tile,
-buckets 32/64/128, every width, inline keys and span-layout key prefixes,
+buckets 32/64/128/512, every width, inline keys and span-layout key prefixes,
 zero / -0.0 / subnormal / non-finite inputs inside full tiles (the careful
 bucket path), all-zero buckets, and input / output pointers that are only
 4-byte aligned (no bulk copies).  Reference: codec.cpp:24-69."""
@@ -53,7 +53,7 @@ def _check(dev, oracle, v, bits, bucket, seed, prefixed, x_off=0, p_off=0):
 
 
 @pytest.mark.parametrize("prefixed", [False, True])
-@pytest.mark.parametrize("bucket", [32, 64, 128])
+@pytest.mark.parametrize("bucket", [32, 64, 128, 512])
 @pytest.mark.parametrize("bits", range(1, 9))
 def test_span_tiles_and_tail(dev, oracle, bits, bucket, prefixed):
     rng = np.random.default_rng(bits * 37 + bucket + prefixed)
@@ -71,7 +71,7 @@ def test_span_lengths(dev, oracle, n, prefixed):
     _check(dev, oracle, v, 4, 128, 42, prefixed)
 
 
-@pytest.mark.parametrize("bucket", [32, 64, 128])
+@pytest.mark.parametrize("bucket", [32, 64, 128, 512])
 @pytest.mark.parametrize("prefixed", [False, True])
 def test_span_special_values_in_full_tiles(dev, oracle, bucket, prefixed):
     """Zeros, -0.0 and subnormals send their bucket down the careful path;
