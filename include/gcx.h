@@ -48,11 +48,13 @@ extern "C" {
 #define GCX_F_NORM_PASS 16u    /* some piece's norms come from the K1a pre-pass (bucket not 32/64/128) */
 #define GCX_F_LANE_GROUP 32u   /* some piece has bucket % 32 == 0 other than 32/64/128 (k_quant32) */
 #define GCX_F_KEY_PREFIX 64u   /* the key table holds seed-independent prefixes (gcx_make_prefix) */
-#define GCX_F_SPAN_DEC 128u    /* every piece is raw or bits<=4 with a power-of-two bucket in
-                                  [128, 4096]: the shuffle-table span decode serves the table */
+#define GCX_F_SPAN_DEC 128u    /* every piece is raw or quantized with a power-of-two bucket in
+                                  [128, 4096]: the span decode serves the table */
 #define GCX_F_SPAN_ENC 256u    /* every quantized piece has the same bits and bucket, bucket in
                                   {32, 64, 128}: the span K1 serves the table; its key runs use
                                   the span key layout (gcx_plan_keys) */
+#define GCX_F_SPAN_DEC_WIDE 512u /* with GCX_F_SPAN_DEC: some piece has bits 5..8 (per-element
+                                   values instead of shuffle tables) */
 #define GCX_F_SPAN_BITS_SHIFT 16 /* with GCX_F_SPAN_ENC: bits at flags[16..19], */
 #define GCX_F_SPAN_LGB_SHIFT 20  /* log2(bucket) at flags[20..23] */
 

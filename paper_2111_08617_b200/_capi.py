@@ -21,6 +21,7 @@ GCX_F_NORM_PASS = 16
 GCX_F_LANE_GROUP = 32
 GCX_F_KEY_PREFIX = 64
 GCX_F_SPAN_DEC = 128
+GCX_F_SPAN_DEC_WIDE = 512
 GCX_TILE = 4096
 
 

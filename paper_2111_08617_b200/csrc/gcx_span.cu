@@ -70,11 +70,13 @@ __global__ void __launch_bounds__(256) k_span_prefix(uint32_t n, uint32_t lgb, u
   }
 }
 
+// WIDE: some piece has widths 5-8 (GCX_F_SPAN_DEC_WIDE; 9-word chunks)
+template <bool WIDE>
 __global__ void __launch_bounds__(32 * kDWarps) k_dspan_pieces(gcx_plan::PlanView pv,
                                                                const uint8_t* __restrict__ msg,
                                                                float* __restrict__ dst, float div,
                                                                float recip, bool pow2) {
-  __shared__ __align__(16) uint32_t words_all[kDWarps][128 * 5];
+  __shared__ __align__(16) uint32_t words_all[kDWarps][128 * (WIDE ? 9 : 5)];
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   uint32_t* words = words_all[warp];
   const uint32_t nw = gridDim.x * kDWarps;
@@ -92,6 +94,10 @@ __global__ void __launch_bounds__(32 * kDWarps) k_dspan_pieces(gcx_plan::PlanVie
       case 2: dspan_piece_tile<2>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
       case 3: dspan_piece_tile<3>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
       case 4: dspan_piece_tile<4>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
+      case 5: if constexpr (WIDE) dspan_piece_tile<5>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
+      case 6: if constexpr (WIDE) dspan_piece_tile<6>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
+      case 7: if constexpr (WIDE) dspan_piece_tile<7>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
+      case 8: if constexpr (WIDE) dspan_piece_tile<8>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
       default: break;
     }
   }
@@ -99,12 +105,13 @@ __global__ void __launch_bounds__(32 * kDWarps) k_dspan_pieces(gcx_plan::PlanVie
 
 // Short tables (a small message): a CTA of 8 warps per tile, warp w decoding
 // chunks 4w..4w+3, so one tile's latency is an eighth of a warp's.
+template <bool WIDE>
 __global__ void __launch_bounds__(32 * kDWarps) k_dspan_pieces_small(gcx_plan::PlanView pv,
                                                                      const uint8_t* __restrict__ msg,
                                                                      float* __restrict__ dst,
                                                                      float div, float recip,
                                                                      bool pow2) {
-  __shared__ __align__(16) uint32_t words[128 * 5 + 4];
+  __shared__ __align__(16) uint32_t words[128 * (WIDE ? 9 : 5) + 4];
   __shared__ gcx_plan::TileCtx ctx_s;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   for (uint32_t t = blockIdx.x; t < pv.ntiles; t += gridDim.x) {
@@ -126,6 +133,10 @@ __global__ void __launch_bounds__(32 * kDWarps) k_dspan_pieces_small(gcx_plan::P
       case 2: dspan_piece_tile<2>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane, c_lo, c_hi); break;
       case 3: dspan_piece_tile<3>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane, c_lo, c_hi); break;
       case 4: dspan_piece_tile<4>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane, c_lo, c_hi); break;
+      case 5: if constexpr (WIDE) dspan_piece_tile<5>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane, c_lo, c_hi); break;
+      case 6: if constexpr (WIDE) dspan_piece_tile<6>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane, c_lo, c_hi); break;
+      case 7: if constexpr (WIDE) dspan_piece_tile<7>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane, c_lo, c_hi); break;
+      case 8: if constexpr (WIDE) dspan_piece_tile<8>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane, c_lo, c_hi); break;
       default: break;
     }
     __syncthreads();
@@ -258,7 +269,7 @@ cudaError_t gcx_span_quantize(const float* x, uint64_t n, int bits, uint64_t buc
 }
 
 bool gcx_span_decode_supported(int bits, uint64_t bucket) {
-  return bits >= 1 && bits <= 4 && bucket >= 128 && bucket <= kWTile && (bucket & (bucket - 1)) == 0;
+  return bits >= 1 && bits <= 8 && bucket >= 128 && bucket <= kWTile && (bucket & (bucket - 1)) == 0;
 }
 
 cudaError_t gcx_span_dequantize(const float* norms, const uint8_t* packed, uint64_t n, int bits,
@@ -300,25 +311,28 @@ bool gcx_span_decode_piece_ok(int bits, uint64_t bucket) {
 
 cudaError_t gcx_span_decode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix,
                                    uint32_t npieces, uint32_t ntiles, const uint8_t* msg,
-                                   float* dst, float divisor, int sms, cudaStream_t st) {
-  static thread_local int occ = 0;
-  if (occ == 0) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dspan_pieces, 32 * kDWarps, 0);
+                                   float* dst, float divisor, bool wide, int sms, cudaStream_t st) {
+  static thread_local int occ[2] = {0, 0};
+  int& o = occ[wide];
+  if (o == 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &o, wide ? k_dspan_pieces<true> : k_dspan_pieces<false>, 32 * kDWarps, 0);
     if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
+    if (o < 1) o = 1;
   }
   gcx_plan::PlanView pv{pieces, tile_prefix, npieces, ntiles, {}};
   int e2 = 0;
   const bool pow2 = std::frexp(divisor, &e2) == 0.5f;
   if (ntiles <= uint32_t(sms) * GCX_SMALL_TILES_PER_SM) {  // short table: CTA per tile
-    k_dspan_pieces_small<<<ntiles, 32 * kDWarps, 0, st>>>(pv, msg, dst, divisor, 1.0f / divisor,
-                                                          pow2);
+    auto fn = wide ? k_dspan_pieces_small<true> : k_dspan_pieces_small<false>;
+    fn<<<ntiles, 32 * kDWarps, 0, st>>>(pv, msg, dst, divisor, 1.0f / divisor, pow2);
     return cudaGetLastError();
   }
   uint32_t grid = (ntiles + kDWarps - 1) / kDWarps;
-  if (grid > uint32_t(sms * occ)) grid = uint32_t(sms * occ);
+  if (grid > uint32_t(sms * o)) grid = uint32_t(sms * o);
   if (grid == 0) grid = 1;
-  k_dspan_pieces<<<grid, 32 * kDWarps, 0, st>>>(pv, msg, dst, divisor, 1.0f / divisor, pow2);
+  auto fn = wide ? k_dspan_pieces<true> : k_dspan_pieces<false>;
+  fn<<<grid, 32 * kDWarps, 0, st>>>(pv, msg, dst, divisor, 1.0f / divisor, pow2);
   return cudaGetLastError();
 }
 

@@ -23,11 +23,12 @@ cudaError_t gcx_span_dequantize(const float* norms, const uint8_t* packed, uint6
                                 uint64_t bucket, float* out, float divisor, int sms,
                                 cudaStream_t st);
 // K3 span decode over a piece table whose pieces are all raw or
-// span-decodable (gcx_plan_tiles sets GCX_F_SPAN_DEC)
+// span-decodable (gcx_plan_tiles sets GCX_F_SPAN_DEC); wide: some piece has
+// widths 5-8 (GCX_F_SPAN_DEC_WIDE)
 bool gcx_span_decode_piece_ok(int bits, uint64_t bucket);
 cudaError_t gcx_span_decode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix,
                                    uint32_t npieces, uint32_t ntiles, const uint8_t* msg,
-                                   float* dst, float divisor, int sms, cudaStream_t st);
+                                   float* dst, float divisor, bool wide, int sms, cudaStream_t st);
 // K1 span over a piece table with GCX_F_SPAN_ENC (bits and log2 bucket in the
 // flags); keys == nullptr: hashed inline; with GCX_F_KEY_PREFIX span-layout
 // prefixes, else a span-layout key table for this seed

@@ -652,6 +652,48 @@ struct SpanPiecesArgs {
   uint32_t nodes, me;
 };
 
+// Widths 5-8: a chunk's table would have F = 2^(bits+1) > 32 entries, so each
+// element's value is computed from its own field instead (dequant_field:
+// RN32(RN64(RN64(norm * level) / s)), signed, then finalize's divisor) — four
+// independent FP64 chains per lane per chunk.  `win` is the lane's 4W-bit
+// window (at most 36 bits: two words).
+//
+// RN32(RN64(nl / s)) for nl = RN64(norm * level) (exact): q0 = RN(nl * RN(1/s))
+// is within 3 ulp of RN64(nl / s) (RN(1/s) and the product each carry a
+// relative error <= 2^-53), so the two round to the same float unless q0's 29
+// dropped bits lie within a few ulp of the halfway point 2^28, or q0 is below
+// the normal float range; only then is dequant_field's correction step taken.
+__device__ __forceinline__ float wide_mag(double nl, double sd, double ys) {
+  const double q0 = __dmul_rn(nl, ys);
+  const uint32_t hi = uint32_t(__double2hiint(q0)), lo = uint32_t(__double2loint(q0));
+  if ((lo & 0x1FFFFFFFu) - 0x0FFFFFF8u < 16u || hi - 1u < 0x380FFFFFu) {  // rare
+    const double q = __fma_rn(__fma_rn(-sd, q0, nl), ys, q0);
+    return f64pos_to_f32_rn(q);
+  }
+  return __double2float_rn(q0);  // nl = 0 (level 0) lands here: +0
+}
+
+template <uint32_t BITS>
+__device__ __forceinline__ void wide_values(uint64_t win, double nd, float div, float recip, bool pow2,
+                                            float (&v)[4]) {
+  constexpr uint32_t W = BITS + 1, S = (1u << BITS) - 1;
+  const double sd = double(S), ys = 1.0 / double(S);  // RN(1/s), as __drcp_rn
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t f = uint32_t(win >> (k * W)) & ((1u << W) - 1u);
+    const float m = wide_mag(__dmul_rn(nd, u32_to_f64(f & S)), sd, ys);
+    v[k] = apply_divisor((f >> BITS) && (f & S) ? -m : m, div, recip, pow2);
+  }
+}
+
+__device__ __forceinline__ uint64_t lane_window2(uint32_t w0, uint32_t w1, uint32_t qsh, bool two) {
+  return (two ? (uint64_t(w1) << 32) | w0 : uint64_t(w0)) >> qsh;
+}
+
+__device__ __forceinline__ uint64_t lane_window(const uint32_t* cw, uint32_t qsh, bool two) {
+  return lane_window2(cw[0], two ? cw[1] : 0u, qsh, two);
+}
+
 // The SRA owner's fold of one tile (collectives.cpp:266-279) straight into
 // the K1 staging slots: row r of the tile (one bucket of 128) is decoded from
 // every peer's payload warp-wide — lane l owns elements 4l..4l+3, the peer's
@@ -660,7 +702,8 @@ struct SpanPiecesArgs {
 // values (f32, the reference's order).  The aggregate is stored swizzled into
 // slot l/8, where the span K1 passes read it.  Row r+1's loads (the peers'
 // norms and packed windows, the owner's raw quad) are issued before row r is
-// folded.  Requires bits <= 4 and bucket 128; nodes <= 8.
+// folded.  Widths 5-8 compute each value from its field (wide_values).
+// Buckets 128 / 512; nodes <= 8.
 template <uint32_t BITS, int LGB>
 __device__ __forceinline__ void fold_tile(const SpanPiecesArgs& A, const gcx_piece& p,
                                           uint32_t start, uint32_t count, float* slots,
@@ -731,6 +774,9 @@ __device__ __forceinline__ void fold_tile(const SpanPiecesArgs& A, const gcx_pie
         x[1] = cur.own.y;
         x[2] = cur.own.z;
         x[3] = cur.own.w;
+      } else if constexpr (F > 32) {  // widths 5-8: per-element values
+        wide_values<BITS>(lane_window2(cur.w0[id], cur.w1[id], qsh, two),
+                          double(__uint_as_float(cur.nu[id])), 1.0f, 1.0f, false, x);
       } else {
         // this lane's entry of peer id's table for the row's bucket (dequant_field)
         const double nl = __dmul_rn(double(__uint_as_float(cur.nu[id])), dl);  // exact
@@ -1101,6 +1147,26 @@ __global__ void __launch_bounds__(32 * kDWarps, GCX_DSPAN_MINB) k_dspan(DspanArg
     __syncwarp();
     float* out = A.out + e0 + 4 * lane;
     const bool vec = (reinterpret_cast<uintptr_t>(out) & 15u) == 0 && full;
+    if constexpr (F > 32) {  // widths 5-8: per-element values (wide_values)
+#pragma unroll 4
+      for (uint32_t c = 0; c < 32; ++c) {
+        if (!full && e0 + c * 128 >= A.n) break;
+        const double nd = double(__uint_as_float(__shfl_sync(0xffffffffu, nreg, c >> BSH)));
+        float v[4];
+        wide_values<BITS>(lane_window(words + c * 4 * W + qw, qsh, two), nd, A.div, A.recip, A.pow2, v);
+        float* o = out + c * 128;
+        if (vec) {
+          __stcs(reinterpret_cast<float4*>(o), make_float4(v[0], v[1], v[2], v[3]));
+        } else {
+          const uint32_t e = e0 + c * 128 + 4 * lane;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (e + k < A.n) __stcs(o + k, v[k]);
+        }
+      }
+      __syncwarp();
+      continue;
+    }
     // batches of 8 chunks: the batch's table entries (one per bucket it
     // touches: RN32(RN64(RN64(norm * level) / s)), /N, signed) are 1..8
     // independent FP64 chains, then the chunks are decoded by shuffles
@@ -1166,6 +1232,10 @@ static inline DspanFn pick_dspan(int bits, uint32_t lgb) {
     case 2: return pick_dspan_lgb<2>(lgb);
     case 3: return pick_dspan_lgb<3>(lgb);
     case 4: return pick_dspan_lgb<4>(lgb);
+    case 5: return pick_dspan_lgb<5>(lgb);
+    case 6: return pick_dspan_lgb<6>(lgb);
+    case 7: return pick_dspan_lgb<7>(lgb);
+    case 8: return pick_dspan_lgb<8>(lgb);
     default: return nullptr;
   }
 }
@@ -1209,6 +1279,26 @@ __device__ __forceinline__ void dspan_piece_tile(const gcx_piece& p, uint32_t st
   __syncwarp();
   float* out = dst + p.src + start + 4 * lane;
   const bool vec = full && (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+  if constexpr (F > 32) {  // widths 5-8: per-element values (wide_values)
+#pragma unroll 4
+    for (uint32_t c = c_lo; c < c_hi; ++c) {
+      if (c * 128 >= count) break;
+      const double nd = double(__uint_as_float(__shfl_sync(0xffffffffu, nreg, c >> bshift)));
+      float v[4];
+      wide_values<BITS>(lane_window(words + c * 4 * W + qw, qsh, two), nd, div, recip, pow2, v);
+      float* o = out + c * 128;
+      if (vec) {
+        __stcs(reinterpret_cast<float4*>(o), make_float4(v[0], v[1], v[2], v[3]));
+      } else {
+        const uint32_t e = c * 128 + 4 * lane;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (e + k < count) __stcs(o + k, v[k]);
+      }
+    }
+    __syncwarp();
+    return;
+  }
   // batches of 8 chunks: 8 independent FP64 chains for the batch's table
   // entries (one per chunk; chunks of one bucket compute the same entry),
   // then 8 chunks decoded by shuffles

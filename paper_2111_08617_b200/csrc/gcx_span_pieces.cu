@@ -32,6 +32,10 @@ static SpanPiecesFn pick_fold_lgb(int bits, bool prefix) {
       case 2: return prefix ? k_span_fold_cta<2, LGB, kKmPrefix, true> : k_span_fold_cta<2, LGB, kKmInline, true>;
       case 3: return prefix ? k_span_fold_cta<3, LGB, kKmPrefix, true> : k_span_fold_cta<3, LGB, kKmInline, true>;
       case 4: return prefix ? k_span_fold_cta<4, LGB, kKmPrefix, true> : k_span_fold_cta<4, LGB, kKmInline, true>;
+      case 5: return prefix ? k_span_fold_cta<5, LGB, kKmPrefix, true> : k_span_fold_cta<5, LGB, kKmInline, true>;
+      case 6: return prefix ? k_span_fold_cta<6, LGB, kKmPrefix, true> : k_span_fold_cta<6, LGB, kKmInline, true>;
+      case 7: return prefix ? k_span_fold_cta<7, LGB, kKmPrefix, true> : k_span_fold_cta<7, LGB, kKmInline, true>;
+      case 8: return prefix ? k_span_fold_cta<8, LGB, kKmPrefix, true> : k_span_fold_cta<8, LGB, kKmInline, true>;
       default: return nullptr;
     }
   }
@@ -188,7 +192,7 @@ cudaError_t gcx_span_encode_pieces(const gcx_piece* pieces, const uint32_t* tile
 bool gcx_span_fold_ok(uint32_t flags, uint32_t nodes) {
   const uint32_t bits = (flags >> GCX_F_SPAN_BITS_SHIFT) & 15u;
   const uint32_t lgb = (flags >> GCX_F_SPAN_LGB_SHIFT) & 15u;
-  return (flags & GCX_F_SPAN_ENC) && bits >= 1 && bits <= 4 && (lgb == 7 || lgb == 9) && nodes >= 2 &&
+  return (flags & GCX_F_SPAN_ENC) && bits >= 1 && bits <= 8 && (lgb == 7 || lgb == 9) && nodes >= 2 &&
          nodes <= 8;
 }
 

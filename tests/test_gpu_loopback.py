@@ -266,3 +266,36 @@ def test_per_rank_non_finite_raises_reference_message(G):
     assert msgs[0] == "non-finite gradient value at index 353"
     m = re.fullmatch(r"non-finite gradient value at index (\d+)", msgs[1])
     assert m and 256 <= int(m.group(1)) < 384, msgs[1]
+
+
+@pytest.mark.parametrize("nodes", [2, 4])
+def test_per_rank_mixed_width_vs_oracle(G, oracle, nodes):
+    """DeviceReducer over a layout mixing widths / buckets (tests/test_gpu_sra
+    MIXED) against the oracle's SRA allreduce on the same inputs, bit for
+    bit, two steps."""
+    import torch
+    from tests.test_gpu_sra import MIXED, mixed_segments
+    segs, d = mixed_segments(MIXED)
+    rng = np.random.default_rng(nodes + 40)
+    xs = [[(rng.standard_normal(d) * 1e-3).astype(np.float32) for _ in range(nodes)]
+          for _ in range(2)]
+    seg_objs = [G.Segment(o, n, G.CodecMode.uncompressed if m == 2 else G.CodecMode.quantize,
+                          b or 4, bk or 128) for o, n, m, b, bk in segs]
+    hub = G.LoopbackHub(nodes)
+
+    def rank(r, stream):
+        red = G.DeviceReducer(hub.transport(r), d, seg_objs)
+        outs = []
+        for step, inputs in enumerate(xs):
+            x = torch.from_numpy(inputs[r]).cuda()
+            red.allreduce(x.data_ptr(), x.data_ptr(), d, 11 + step, G.ReduceOp.average,
+                          stream.cuda_stream)
+            red.poll(True)
+            outs.append(x.cpu().numpy())
+        return outs
+
+    res = run_ranks(nodes, rank)
+    for step, inputs in enumerate(xs):
+        want = oracle.sra_allreduce(inputs, segs, 11 + step, True)
+        for r in range(nodes):
+            assert (res[r][step].view(np.uint32) == want.view(np.uint32)).all(), (step, r)

@@ -150,12 +150,13 @@ def test_span_seeds_differ_only_in_keys(dev, oracle):
         assert (packed.cpu().numpy()[: wp.size] == wp).all(), seed
 
 
-@pytest.mark.parametrize("bits", [1, 2, 3, 4])
+@pytest.mark.parametrize("bits", range(1, 9))
 @pytest.mark.parametrize("bucket", [128, 256, 512, 1024, 2048, 4096])
 def test_span_decode_vs_oracle(dev, oracle, bits, bucket):
-    """K3 span decode (shuffle tables, one chunk of 128 per bucket slice):
-    bit-exact dequantize (codec.cpp:71-95) over full tiles, a ragged tile and
-    an output pointer that is only 4-byte aligned."""
+    """K3 span decode (one chunk of 128 per bucket slice; shuffle tables for
+    widths 1-4, per-element values for 5-8): bit-exact dequantize
+    (codec.cpp:71-95) over full tiles, a ragged tile and an output pointer
+    that is only 4-byte aligned."""
     rng = np.random.default_rng(bits * 100 + bucket)
     for n in (4096 * 11 + int(rng.integers(1, 4096)), 100, 4096, 129):
         v = (rng.standard_normal(n) * 10.0 ** rng.integers(-20, 20)).astype(np.float32)
@@ -176,3 +177,22 @@ def test_span_decode_vs_oracle(dev, oracle, bits, bucket):
             got = obuf.cpu().numpy()
             assert (got[off:off + n].view(np.uint32) == want.view(np.uint32)).all(), (n, off)
             assert (got[off + n:] == 7.0).all() and (got[:off] == 7.0).all()
+
+
+@pytest.mark.parametrize("bits", [5, 8])
+def test_span_decode_tiny_norms(dev, oracle, bits):
+    """Values whose dequantized magnitudes fall below the normal float range
+    (the wide decode's exact correction + slow conversion path)."""
+    rng = np.random.default_rng(bits)
+    n = 4096 * 3 + 700
+    v = (rng.standard_normal(n) * 1e-38).astype(np.float32)
+    v[:2048] *= np.float32(1e-3)  # subnormal inputs
+    wn, wp = oracle.quantize(v, bits, 512, 5)
+    want = oracle.dequantize(wn, wp, n, bits, 512)
+    from paper_2111_08617_b200 import _capi
+    pk = np.zeros(_capi.packed_capacity(n, bits), np.uint8)
+    pk[: wp.size] = wp
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    dev.dequantize(torch.from_numpy(wn).cuda(), torch.from_numpy(pk).cuda(), n, bits, 512, out=out)
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy().view(np.uint32) == want.view(np.uint32)).all()

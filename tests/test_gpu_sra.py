@@ -201,3 +201,30 @@ def test_ring_and_tree_vs_compiled_reference(g, topology):
         assert tr.decompress_calls == ctr["decompress_calls"], (trial, ctr)
         assert tr.message_count == ctr["message_count"] and tr.rounds == ctr["rounds"], ctr
         assert tr.max_compress_depth == ctr["max_compress_depth"], (trial, ctr)
+
+
+MIXED = [(2, 128, 70_000), (8, 128, 90_001), (3, 128, 66_000), (0, 0, 5_000), (4, 512, 80_000),
+         (5, 128, 70_000), (4, 128, 100), (6, 64, 70_000), (1, 1024, 70_000), (4, 128, 75_000),
+         (2, 128, 600_000)]
+
+
+def mixed_segments(classes):
+    segs, off = [], 0
+    for bits, bucket, n in classes:
+        segs.append((off, n, 2 if bits == 0 else 0, bits, bucket))
+        off += n
+    return segs, off
+
+
+@pytest.mark.parametrize("nodes", [2, 3, 8])
+def test_mixed_width_layout_vs_oracle(g, oracle, nodes):
+    """A 1.3 M-element layout mixing (bits, bucket) classes the way the
+    adaptive planner's per-layer widths do (plus raw and a 100-element
+    piece): the oracle's SRA, bit for bit."""
+    rng = np.random.default_rng(nodes)
+    segs, d = mixed_segments(MIXED)
+    inputs = [(rng.standard_normal(d) * 1e-3).astype(np.float32) for _ in range(nodes)]
+    want = oracle.sra_allreduce(inputs, segs, 0xC4, True)
+    res = g.allreduce(_request(g, inputs, segs, 0xC4, True), nodes)
+    for o in res.outputs:
+        assert (o.view(np.uint32) == want.view(np.uint32)).all()
