@@ -41,6 +41,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -71,33 +72,45 @@ __global__ void __launch_bounds__(256) k_span_prefix(uint32_t n, uint32_t lgb, u
 }
 
 // WIDE: some piece has widths 5-8 (GCX_F_SPAN_DEC_WIDE; 9-word chunks)
+// A work item is 1/2^lgs of a tile (chunks [c_lo, c_hi)): when the table has
+// about one tile per warp, a tile's decode is a chain of dependent latencies
+// (locate, stage, 32 chunks) that splitting shortens.
 template <bool WIDE>
 __global__ void __launch_bounds__(32 * kDWarps) k_dspan_pieces(gcx_plan::PlanView pv,
                                                                const uint8_t* __restrict__ msg,
                                                                float* __restrict__ dst, float div,
-                                                               float recip, bool pow2) {
+                                                               float recip, bool pow2, uint32_t lgs) {
   __shared__ __align__(16) uint32_t words_all[kDWarps][128 * (WIDE ? 9 : 5)];
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   uint32_t* words = words_all[warp];
-  const uint32_t nw = gridDim.x * kDWarps;
-  for (uint32_t t = blockIdx.x * kDWarps + warp; t < pv.ntiles; t += nw) {
+  const uint32_t nw = gridDim.x * kDWarps, nitems = pv.ntiles << lgs, cp = 32u >> lgs;
+  for (uint32_t u = blockIdx.x * kDWarps + warp; u < nitems; u += nw) {
     gcx_plan::TileCtx c;
-    gcx_plan::locate_warp(pv, t, c);
+    gcx_plan::locate_warp(pv, u >> lgs, c);
     const gcx_piece& p = c.p;
+    const uint32_t c_lo = (u & ((1u << lgs) - 1u)) * cp, c_hi = c_lo + cp;
+    if (c_lo * 128u >= c.count) continue;
     switch (p.bits) {
       case 0: {  // raw piece: f32 payload at p.norms, divided (finalize's average)
-        raw_copy(reinterpret_cast<const float*>(msg + p.norms) + c.start, dst + p.src + c.start,
-                 c.count, div, recip, pow2, lane, 32);
+        const uint32_t e0 = c.start + c_lo * 128u;
+        raw_copy(reinterpret_cast<const float*>(msg + p.norms) + e0, dst + p.src + e0,
+                 min(c.count - c_lo * 128u, cp * 128u), div, recip, pow2, lane, 32);
         break;
       }
-      case 1: dspan_piece_tile<1>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
-      case 2: dspan_piece_tile<2>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
-      case 3: dspan_piece_tile<3>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
-      case 4: dspan_piece_tile<4>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
-      case 5: if constexpr (WIDE) dspan_piece_tile<5>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
-      case 6: if constexpr (WIDE) dspan_piece_tile<6>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
-      case 7: if constexpr (WIDE) dspan_piece_tile<7>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
-      case 8: if constexpr (WIDE) dspan_piece_tile<8>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane); break;
+#define GCX_DSPAN_CASE(B) \
+      case B: dspan_piece_tile<B>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane, c_lo, c_hi); break;
+      GCX_DSPAN_CASE(1)
+      GCX_DSPAN_CASE(2)
+      GCX_DSPAN_CASE(3)
+      GCX_DSPAN_CASE(4)
+#undef GCX_DSPAN_CASE
+#define GCX_DSPAN_CASE(B) \
+      case B: if constexpr (WIDE) dspan_piece_tile<B>(p, c.start, c.count, msg, dst, div, recip, pow2, words, lane, c_lo, c_hi); break;
+      GCX_DSPAN_CASE(5)
+      GCX_DSPAN_CASE(6)
+      GCX_DSPAN_CASE(7)
+      GCX_DSPAN_CASE(8)
+#undef GCX_DSPAN_CASE
       default: break;
     }
   }
@@ -328,11 +341,24 @@ cudaError_t gcx_span_decode_pieces(const gcx_piece* pieces, const uint32_t* tile
     fn<<<ntiles, 32 * kDWarps, 0, st>>>(pv, msg, dst, divisor, 1.0f / divisor, pow2);
     return cudaGetLastError();
   }
-  uint32_t grid = (ntiles + kDWarps - 1) / kDWarps;
+  // wide tables with fewer than 2 tiles per resident warp decode half tiles
+  // (C3 8b/512 N = 8: -6 % per step); narrow tables measured no gain from
+  // splitting (1/2/4/8 parts on C2 / C3 2b).  GCX_DSPAN_SPLIT=k forces 2^k
+  // parts (measurement)
+  const uint64_t slots = uint64_t(sms) * uint64_t(o) * kDWarps;
+  uint32_t lgs = wide && uint64_t(ntiles) < 2 * slots ? 1u : 0u;
+  static const int forced = [] {
+    const char* e = std::getenv("GCX_DSPAN_SPLIT");
+    return e != nullptr ? std::atoi(e) : -1;
+  }();
+  if (forced >= 0 && forced <= 3) lgs = uint32_t(forced);
+  if ((uint64_t(ntiles) << lgs) > 0xFFFFFFFFull) lgs = 0;
+  const uint64_t items = uint64_t(ntiles) << lgs;
+  uint32_t grid = uint32_t((items + kDWarps - 1) / kDWarps);
   if (grid > uint32_t(sms * o)) grid = uint32_t(sms * o);
   if (grid == 0) grid = 1;
   auto fn = wide ? k_dspan_pieces<true> : k_dspan_pieces<false>;
-  fn<<<grid, 32 * kDWarps, 0, st>>>(pv, msg, dst, divisor, 1.0f / divisor, pow2);
+  fn<<<grid, 32 * kDWarps, 0, st>>>(pv, msg, dst, divisor, 1.0f / divisor, pow2, lgs);
   return cudaGetLastError();
 }
 
