@@ -765,6 +765,20 @@ __device__ __forceinline__ void fold_tile(const SpanPiecesArgs& A, const gcx_pie
     RowLoads nxt;
     if (r + rstep < r1) load_row(r + rstep, nxt);
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    // every peer's table entry first (absent peers give 0), unconditionally:
+    // eight independent FP64 chains the scheduler can overlap
+    float entry[8];
+    if constexpr (F <= 32) {
+#pragma unroll
+      for (uint32_t id = 0; id < 8; ++id) {
+        // this lane's entry of peer id's table for the row's bucket (dequant_field)
+        const double nl = __dmul_rn(double(__uint_as_float(cur.nu[id])), dl);  // exact
+        const double q0 = __dmul_rn(nl, ys);
+        const double q = __fma_rn(__fma_rn(-sd, q0, nl), ys, q0);
+        const float m = __double2float_rn(q);
+        entry[id] = level == 0 ? 0.0f : (sign ? -m : m);
+      }
+    }
 #pragma unroll
     for (uint32_t id = 0; id < 8; ++id) {
       if (id >= nodes) break;
@@ -778,15 +792,9 @@ __device__ __forceinline__ void fold_tile(const SpanPiecesArgs& A, const gcx_pie
         wide_values<BITS>(lane_window2(cur.w0[id], cur.w1[id], qsh, two),
                           double(__uint_as_float(cur.nu[id])), 1.0f, 1.0f, false, x);
       } else {
-        // this lane's entry of peer id's table for the row's bucket (dequant_field)
-        const double nl = __dmul_rn(double(__uint_as_float(cur.nu[id])), dl);  // exact
-        const double q0 = __dmul_rn(nl, ys);
-        const double q = __fma_rn(__fma_rn(-sd, q0, nl), ys, q0);
-        const float m = __double2float_rn(q);
-        const float entry = level == 0 ? 0.0f : (sign ? -m : m);
         const uint32_t win = two ? __funnelshift_r(cur.w0[id], cur.w1[id], qsh) : (cur.w0[id] >> qsh);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) x[k] = __shfl_sync(0xffffffffu, entry, (win >> (k * W)) & (F - 1u));
+        for (int k = 0; k < 4; ++k) x[k] = __shfl_sync(0xffffffffu, entry[id], (win >> (k * W)) & (F - 1u));
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) acc[k] = id == 0 ? x[k] : __fadd_rn(acc[k], x[k]);
