@@ -6,6 +6,7 @@
 //                              reference's single-process allreduce(req, net))
 //   DeviceReducer              one rank per GPU, NCCL grouped send/recv over
 //                              NVLink for the two exchange rounds.
+#include <nvtx3/nvToolsExt.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -1146,8 +1147,20 @@ DeviceReducer::DeviceReducer(Transport& transport, std::size_t d, std::vector<Se
 
 DeviceReducer::~DeviceReducer() = default;
 
+namespace {
+// NVTX range over one phase of the per-rank step (host-side issue; nsys /
+// ncu --nvtx show them around the phase's launches)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
+
 void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_seed, ReduceOp op,
                               void* stream) {
+  NvtxRange step_range("gcx.sra.step");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const std::size_t N = layout_.nodes, me = std::size_t(transport_.rank()), d = layout_.d;
   if (N == 1) {  // collectives.cpp:479-486: identity, nothing compressed
@@ -1167,23 +1180,38 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
   auto* keys = I.keys.get<unsigned long long>();
   // K1: my share of every other owner's chunk, seed hop_seed(step, 0, me)
   // (collectives.cpp:252-253)
-  encode(I.blob, I.send, hop_seed(step_seed, 0, me), in, I.send_buf.get<std::uint8_t>(), keys,
-         bad, st, I.prefix_send.get<unsigned long long>());
+  {
+    NvtxRange r("gcx.sra.k1_scatter");
+    encode(I.blob, I.send, hop_seed(step_seed, 0, me), in, I.send_buf.get<std::uint8_t>(), keys,
+           bad, st, I.prefix_send.get<unsigned long long>());
+  }
   // round 1: all-to-all of compressed chunks (collectives.cpp:255, :264)
-  transport_.exchange(I.sends[0], I.recvs[0], st);
+  {
+    NvtxRange r("gcx.sra.exchange_scatter");
+    transport_.exchange(I.sends[0], I.recvs[0], st);
+  }
   // K2: ascending-id fold into out, then re-encode with the hop-1 seed
   // (collectives.cpp:266-284)
   std::uint8_t* bcast = I.gather_buf.get<std::uint8_t>() + layout_.gather_offset[me];
-  owner_step(I.blob, I.own, I.recv_buf.get<std::uint8_t>(), I.recv_stride, in, N, me,
-             hop_seed(step_seed, 1, me), bcast, out, keys, bad + 1, st,
-             I.prefix_own.get<unsigned long long>());
+  {
+    NvtxRange r("gcx.sra.owner_fold_encode");
+    owner_step(I.blob, I.own, I.recv_buf.get<std::uint8_t>(), I.recv_stride, in, N, me,
+               hop_seed(step_seed, 1, me), bcast, out, keys, bad + 1, st,
+               I.prefix_own.get<unsigned long long>());
+  }
   // round 2: variable-size all-gather of the owners' compressed aggregates
   // (collectives.cpp:289, :297)
-  transport_.exchange(I.sends[1], I.recvs[1], st);
+  {
+    NvtxRange r("gcx.sra.exchange_allgather");
+    transport_.exchange(I.sends[1], I.recvs[1], st);
+  }
   // K3: decode every owner's chunk (own included) (+ average)
-  gcx_check(gcx_decode_pieces(I.blob.pieces(I.dec), I.blob.prefix(I.dec),
-                              std::uint32_t(I.dec.pieces.size()), I.dec.ntiles, I.dec.flags,
-                              I.gather_buf.get<std::uint8_t>(), out, divisor, st));
+  {
+    NvtxRange r("gcx.sra.k3_decode");
+    gcx_check(gcx_decode_pieces(I.blob.pieces(I.dec), I.blob.prefix(I.dec),
+                                std::uint32_t(I.dec.pieces.size()), I.dec.ntiles, I.dec.flags,
+                                I.gather_buf.get<std::uint8_t>(), out, divisor, st));
+  }
   cuda_check(cudaMemcpyAsync(I.host_bad, I.bad.get(), 16, cudaMemcpyDeviceToHost, st), "D2H");
   cuda_check(cudaEventRecord(I.done, st), "event record");
   I.pending = true;
