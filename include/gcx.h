@@ -55,6 +55,11 @@ extern "C" {
                                   the span key layout (gcx_plan_keys) */
 #define GCX_F_SPAN_DEC_WIDE 512u /* with GCX_F_SPAN_DEC: some piece has bits 5..8 (per-element
                                    values instead of shuffle tables) */
+#define GCX_F_SEED_DEVICE 1024u /* the launch `seed` argument carries the device address of
+                                   a uint64 seed written earlier on the stream
+                                   (gcx_sra_step_seeds): a step captured in a CUDA graph
+                                   replays with fresh seeds.  Span tables only
+                                   (GCX_F_SPAN_ENC); other tables are rejected. */
 #define GCX_F_SPAN_BITS_SHIFT 16 /* with GCX_F_SPAN_ENC: bits at flags[16..19], */
 #define GCX_F_SPAN_LGB_SHIFT 20  /* log2(bucket) at flags[20..23] */
 
@@ -159,6 +164,16 @@ int gcx_make_key_prefix(const gcx_keygroup* groups, uint32_t ngroups, uint64_t t
                         unsigned long long* prefix, void* stream);
 int gcx_make_keys_prefixed(uint64_t total, uint64_t seed, const unsigned long long* prefix,
                            unsigned long long* keys, void* stream);
+/* make_keys_prefixed with the seed read from device memory (*seed_dev) */
+int gcx_make_keys_prefixed_dev(uint64_t total, const unsigned long long* seed_dev,
+                               const unsigned long long* prefix, unsigned long long* keys,
+                               void* stream);
+/* Per-step SRA seeds on the device (a graph-replayable step): state[0] =
+ * base seed, state[1] = step, state[2] = buffer index, state[3] = node id.
+ * Writes state[4] = hop_seed(S, 0, node), state[5] = hop_seed(S, 1, node)
+ * with S = hash_combine(hash_combine(base, step), buffer) (engine.cpp:208-209,
+ * collectives.cpp:252-253, :283), then state[1] = step + 1. */
+int gcx_sra_step_seeds(unsigned long long* state, void* stream);
 int gcx_decode_pieces(const gcx_piece* pieces, const uint32_t* tile_prefix, uint32_t npieces,
                       uint32_t ntiles, uint32_t flags, const uint8_t* msg, float* dst,
                       float divisor, void* stream);

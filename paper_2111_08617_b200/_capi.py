@@ -20,6 +20,8 @@ GCX_F_ODD_BUCKETS = 8
 GCX_F_NORM_PASS = 16
 GCX_F_LANE_GROUP = 32
 GCX_F_KEY_PREFIX = 64
+GCX_F_SPAN_ENC = 256
+GCX_F_SEED_DEVICE = 1024
 GCX_F_SPAN_DEC = 128
 GCX_F_SPAN_DEC_WIDE = 512
 GCX_TILE = 4096
@@ -84,6 +86,8 @@ _decl("gcx_plan_keys", i64, C.POINTER(Piece), u32, C.POINTER(KeyGroup), u32, C.P
 _decl("gcx_make_keys", i32, vp, u32, u64, u64, vp, vp)
 _decl("gcx_make_key_prefix", i32, vp, u32, u64, vp, vp)
 _decl("gcx_make_keys_prefixed", i32, u64, u64, vp, vp, vp)
+_decl("gcx_make_keys_prefixed_dev", i32, u64, vp, vp, vp, vp)
+_decl("gcx_sra_step_seeds", i32, vp, vp)
 _decl("gcx_fold_pieces", i32, vp, vp, u32, u32, u32, vp, u64, vp, u32, u32, vp, vp)
 _decl("gcx_sra_fold_encode", i32, vp, vp, u32, u32, u32, vp, u64, vp, u32, u32, u64, vp, vp, vp,
       vp, vp)
@@ -103,6 +107,7 @@ EXPORTS = ["gcx_version", "gcx_last_error", "gcx_compressed_size", "gcx_packed_b
            "gcx_sra_reduce", "gcx_sra_fold_encode", "gcx_hash_bench", "gcx_device_info", "gcx_plan_keys",
            "gcx_make_keys", "gcx_fold_pieces", "gcx_prefix_slots", "gcx_make_prefix",
            "gcx_quantize_prefixed", "gcx_make_key_prefix", "gcx_make_keys_prefixed",
+           "gcx_make_keys_prefixed_dev", "gcx_sra_step_seeds",
            "gcx_stats_accumulate", "gcx_add_f32", "gcx_wire_layout", "gcx_frame_pieces",
            "gcx_unframe_pieces"]
 

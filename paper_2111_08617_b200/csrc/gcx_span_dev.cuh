@@ -641,6 +641,7 @@ struct SpanPiecesArgs {
   gcx_plan::PlanView pv;
   uint32_t flags;
   uint64_t seed;
+  const unsigned long long* seed_dev;  // GCX_F_SEED_DEVICE: the launch seed, read on the device
   const float* src;      // the input (FOLD: the owner's raw values)
   uint8_t* msg;          // the message written (FOLD: the owner's broadcast message)
   const uint32_t* keys;  // span-layout prefix words or nullptr (inline)
@@ -651,6 +652,13 @@ struct SpanPiecesArgs {
   uint64_t slot_stride;
   uint32_t nodes, me;
 };
+
+// The table's launch seed: a kernel argument, or (GCX_F_SEED_DEVICE: a step
+// replayed from a CUDA graph) a word in device memory written earlier on the
+// stream (gcx_sra_step_seeds)
+__device__ __forceinline__ uint64_t launch_seed(const SpanPiecesArgs& A) {
+  return A.seed_dev != nullptr ? *A.seed_dev : A.seed;
+}
 
 // Widths 5-8: a chunk's table would have F = 2^(bits+1) > 32 entries, so each
 // element's value is computed from its own field instead (dequant_field:
@@ -960,7 +968,7 @@ __global__ void __launch_bounds__(32 * kWarps, 1) k_span_pieces(SpanPiecesArgs A
       cur = nxt;
       continue;
     }
-    const uint64_t seed = piece_seeds ? p.seed : A.seed;
+    const uint64_t seed = piece_seeds ? p.seed : launch_seed(A);
     const uint32_t s_lo = uint32_t(seed), s_hi = uint32_t(seed >> 32);
     const bool full = cur.count == kWTile;
     const uint32_t i_lane = cur.start + lane * kSpan;  // piece-local first element of the row
@@ -1412,7 +1420,7 @@ __global__ void __launch_bounds__(32 * kFoldWarps, GCX_FOLD_MINB) k_span_fold_ct
       __syncthreads();
       continue;
     }
-    const uint64_t seed = (A.flags & GCX_F_PIECE_SEEDS) ? p.seed : A.seed;
+    const uint64_t seed = (A.flags & GCX_F_PIECE_SEEDS) ? p.seed : launch_seed(A);
     const uint32_t s_lo = uint32_t(seed), s_hi = uint32_t(seed >> 32);
     // A: fold (or stage) rows 8w..8w+7
     if constexpr (FOLD) {

@@ -134,6 +134,8 @@ static cudaError_t span_small_encode(const gcx_piece* pieces, const uint32_t* ti
   a.pv = gcx_plan::PlanView{pieces, tile_prefix, npieces, ntiles, {}};
   a.flags = flags;
   a.seed = seed;
+  a.seed_dev = (flags & GCX_F_SEED_DEVICE) ? reinterpret_cast<const unsigned long long*>(seed)
+                                           : nullptr;
   a.src = src;
   a.msg = msg;
   a.keys = reinterpret_cast<const uint32_t*>(keys);
@@ -174,6 +176,8 @@ cudaError_t gcx_span_encode_pieces(const gcx_piece* pieces, const uint32_t* tile
   a.pv = gcx_plan::PlanView{pieces, tile_prefix, npieces, ntiles, {}};
   a.flags = flags;
   a.seed = seed;
+  a.seed_dev = (flags & GCX_F_SEED_DEVICE) ? reinterpret_cast<const unsigned long long*>(seed)
+                                           : nullptr;
   a.src = src;
   a.msg = msg;
   a.keys = reinterpret_cast<const uint32_t*>(keys);
@@ -224,6 +228,8 @@ cudaError_t gcx_span_fold_encode(const gcx_piece* pieces, const uint32_t* tile_p
   a.pv = gcx_plan::PlanView{pieces, tile_prefix, npieces, ntiles, {}};
   a.flags = flags | (prefix != nullptr ? GCX_F_KEY_PREFIX : 0u);
   a.seed = seed;
+  a.seed_dev = (flags & GCX_F_SEED_DEVICE) ? reinterpret_cast<const unsigned long long*>(seed)
+                                           : nullptr;
   a.src = own;
   a.msg = bcast;
   a.keys = reinterpret_cast<const uint32_t*>(prefix);

@@ -363,6 +363,10 @@ PYBIND11_MODULE(_gcomm, m) {
           py::arg("op"), py::arg("stream") = 0)
       .def("poll", &collectives::DeviceReducer::poll, py::arg("wait") = true,
            py::call_guard<py::gil_scoped_release>())
+      .def("use_device_seeds", &collectives::DeviceReducer::use_device_seeds,
+           py::arg("base_seed"), py::arg("buffer"), py::arg("next_step"))
+      .def("device_step", &collectives::DeviceReducer::device_step)
+      .def("check_replay", &collectives::DeviceReducer::check_replay)
       .def("elements", &collectives::DeviceReducer::elements)
       .def("trace", &collectives::DeviceReducer::trace)
       .def("device_bytes_sent", &collectives::DeviceReducer::device_bytes_sent)

@@ -368,24 +368,33 @@ bool onestep(const Table& t) {
 
 bool onestep_table(const Table& t) { return onestep(t); }
 
+// seed_dev (a graph-replayable step): the seed is read on the device from
+// *seed_dev (GCX_F_SEED_DEVICE), span tables with key prefixes only.
 void encode(const TableBlob& blob, const Table& t, std::uint64_t seed, const float* src,
             std::uint8_t* msg, unsigned long long* keys, unsigned long long* bad,
-            cudaStream_t st, const unsigned long long* key_prefix = nullptr) {
+            cudaStream_t st, const unsigned long long* key_prefix = nullptr,
+            const unsigned long long* seed_dev = nullptr) {
   const bool use_keys = keys != nullptr && t.key_len > 0;
+  const std::uint32_t fdev = seed_dev != nullptr ? GCX_F_SEED_DEVICE : 0u;
+  const std::uint64_t sarg = seed_dev != nullptr ? reinterpret_cast<std::uint64_t>(seed_dev) : seed;
   if (use_keys && key_prefix != nullptr && onestep(t)) {
     gcx_check(gcx_encode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
-                                t.ntiles, t.flags | GCX_F_KEY_PREFIX, seed, src, msg, key_prefix,
-                                bad, st));
+                                t.ntiles, t.flags | GCX_F_KEY_PREFIX | fdev, sarg, src, msg,
+                                key_prefix, bad, st));
     return;
   }
-  if (use_keys && key_prefix != nullptr)
+  if (use_keys && key_prefix != nullptr && seed_dev != nullptr)
+    gcx_check(gcx_make_keys_prefixed_dev(t.key_len, seed_dev, key_prefix, keys, st));
+  else if (use_keys && key_prefix != nullptr)
     gcx_check(gcx_make_keys_prefixed(t.key_len, seed, key_prefix, keys, st));
+  else if (use_keys && seed_dev != nullptr)
+    throw std::invalid_argument("device-resident seeds need the table's key prefixes");
   else if (use_keys)
     gcx_check(gcx_make_keys(blob.groups(t), std::uint32_t(t.groups.size()), t.key_len, seed, keys,
                             st));
   gcx_check(gcx_encode_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
-                              t.ntiles, t.flags, seed, src, msg, use_keys ? keys : nullptr, bad,
-                              st));
+                              t.ntiles, t.flags | fdev, sarg, src, msg, use_keys ? keys : nullptr,
+                              bad, st));
 }
 
 // The owner's fold + hop-1 re-encode (collectives.cpp:266-284): one fused
@@ -394,19 +403,22 @@ void encode(const TableBlob& blob, const Table& t, std::uint64_t seed, const flo
 void owner_step(const TableBlob& blob, const Table& t, const std::uint8_t* recv,
                 std::uint64_t slot_stride, const float* own, std::size_t nodes, std::size_t me,
                 std::uint64_t seed, std::uint8_t* bcast, float* out, unsigned long long* keys,
-                unsigned long long* bad, cudaStream_t st, const unsigned long long* key_prefix) {
+                unsigned long long* bad, cudaStream_t st, const unsigned long long* key_prefix,
+                const unsigned long long* seed_dev = nullptr) {
   const bool pre = key_prefix != nullptr && t.key_len > 0;
   if ((t.flags & GCX_F_SPAN_ENC) && nodes <= 8) {
-    gcx_check(gcx_sra_fold_encode(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
-                                  t.ntiles, t.flags | (pre ? GCX_F_KEY_PREFIX : 0u), recv,
-                                  slot_stride, own, std::uint32_t(nodes), std::uint32_t(me), seed,
-                                  bcast, out, pre ? key_prefix : nullptr, bad, st));
+    gcx_check(gcx_sra_fold_encode(
+        blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()), t.ntiles,
+        t.flags | (pre ? GCX_F_KEY_PREFIX : 0u) | (seed_dev != nullptr ? GCX_F_SEED_DEVICE : 0u),
+        recv, slot_stride, own, std::uint32_t(nodes), std::uint32_t(me),
+        seed_dev != nullptr ? reinterpret_cast<std::uint64_t>(seed_dev) : seed, bcast, out,
+        pre ? key_prefix : nullptr, bad, st));
     return;
   }
   gcx_check(gcx_fold_pieces(blob.pieces(t), blob.prefix(t), std::uint32_t(t.pieces.size()),
                             t.ntiles, t.flags, recv, slot_stride, own, std::uint32_t(nodes),
                             std::uint32_t(me), out, st));
-  encode(blob, t, seed, out, bcast, keys, bad, st, key_prefix);
+  encode(blob, t, seed, out, bcast, keys, bad, st, key_prefix, seed_dev);
 }
 
 Table shifted(const std::vector<gcx_piece>& src, std::uint64_t delta) {
@@ -986,6 +998,10 @@ void LoopbackHub::exchange(int rank, const std::vector<PeerTransfer>& sends,
                            const std::vector<PeerTransfer>& recvs, void* stream) {
   Impl& I = *impl_;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cuda_check(cudaStreamIsCapturing(st, &cap), "cudaStreamIsCapturing");
+  if (cap != cudaStreamCaptureStatusNone)  // its rounds are host rendezvous between threads
+    throw std::logic_error("the loopback transport cannot be captured in a CUDA graph");
   const std::size_t me = std::size_t(rank);
   if (!I.ready[me]) {
     cuda_check(cudaEventCreateWithFlags(&I.ready[me], cudaEventDisableTiming), "event");
@@ -1088,6 +1104,10 @@ struct DeviceReducer::Impl {
   unsigned long long* host_bad = nullptr;
   cudaEvent_t done = nullptr;
   bool pending = false;
+  // device-resident step seeds (use_device_seeds): {base, step, buffer, me,
+  // hop-0 seed, hop-1 seed}, advanced on the device every call
+  DeviceBuffer seed_state;
+  bool dev_seeds = false;
   ~Impl() {
     if (host_bad) cudaFreeHost(host_bad);
     if (done) cudaEventDestroy(done);
@@ -1170,6 +1190,18 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
   }
   Impl& I = *impl_;
   const float divisor = op == ReduceOp::average ? float(N) : 1.0f;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cuda_check(cudaStreamIsCapturing(st, &cap), "cudaStreamIsCapturing");
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  if (capturing && !I.dev_seeds)  // a replay would repeat this step's keys
+    throw std::logic_error("capturing a DeviceReducer step needs use_device_seeds()");
+  const unsigned long long* seed0 = nullptr;
+  const unsigned long long* seed1 = nullptr;
+  if (I.dev_seeds) {  // step_seed is not used: the device counter supplies it
+    gcx_check(gcx_sra_step_seeds(I.seed_state.get<unsigned long long>(), st));
+    seed0 = I.seed_state.get<unsigned long long>() + 4;
+    seed1 = seed0 + 1;
+  }
   cuda_check(cudaMemsetAsync(I.bad.get(), 0xFF, 16, st), "memset");
   if (I.flags & GCX_F_NEEDS_ZERO) {
     cuda_check(cudaMemsetAsync(I.send_buf.get(), 0, I.send_buf.size(), st), "memset");
@@ -1183,7 +1215,7 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
   {
     NvtxRange r("gcx.sra.k1_scatter");
     encode(I.blob, I.send, hop_seed(step_seed, 0, me), in, I.send_buf.get<std::uint8_t>(), keys,
-           bad, st, I.prefix_send.get<unsigned long long>());
+           bad, st, I.prefix_send.get<unsigned long long>(), seed0);
   }
   // round 1: all-to-all of compressed chunks (collectives.cpp:255, :264)
   {
@@ -1197,7 +1229,7 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
     NvtxRange r("gcx.sra.owner_fold_encode");
     owner_step(I.blob, I.own, I.recv_buf.get<std::uint8_t>(), I.recv_stride, in, N, me,
                hop_seed(step_seed, 1, me), bcast, out, keys, bad + 1, st,
-               I.prefix_own.get<unsigned long long>());
+               I.prefix_own.get<unsigned long long>(), seed1);
   }
   // round 2: variable-size all-gather of the owners' compressed aggregates
   // (collectives.cpp:289, :297)
@@ -1213,8 +1245,45 @@ void DeviceReducer::allreduce(const float* in, float* out, std::uint64_t step_se
                                 I.gather_buf.get<std::uint8_t>(), out, divisor, st));
   }
   cuda_check(cudaMemcpyAsync(I.host_bad, I.bad.get(), 16, cudaMemcpyDeviceToHost, st), "D2H");
+  if (capturing) return;  // each replay copies its flags; check_replay() reads them
   cuda_check(cudaEventRecord(I.done, st), "event record");
   I.pending = true;
+}
+
+void DeviceReducer::use_device_seeds(std::uint64_t base_seed, std::uint64_t buffer,
+                                     std::uint64_t next_step) {
+  const std::size_t N = layout_.nodes;
+  if (N == 1) return;  // identity: no keys drawn
+  Impl& I = *impl_;
+  if (!(I.send.flags & GCX_F_SPAN_ENC) || !(I.own.flags & GCX_F_SPAN_ENC) || N > 8)
+    throw std::invalid_argument(
+        "device-resident seeds need span tables (one bits/bucket in {32, 64, 128, 512}) and "
+        "at most 8 nodes");
+  if (I.seed_state.size() == 0) I.seed_state.reset(8 * 8);
+  const std::uint64_t h[6] = {base_seed, next_step, buffer, std::uint64_t(transport_.rank()), 0,
+                              0};
+  cuda_check(cudaMemcpy(I.seed_state.get(), h, sizeof(h), cudaMemcpyHostToDevice), "H2D");
+  I.dev_seeds = true;
+}
+
+std::uint64_t DeviceReducer::device_step() const {
+  const Impl& I = *impl_;
+  if (!I.dev_seeds) return 0;
+  std::uint64_t h[2] = {0, 0};
+  cuda_check(cudaMemcpy(h, I.seed_state.get(), sizeof(h), cudaMemcpyDeviceToHost), "D2H");
+  return h[1];
+}
+
+void DeviceReducer::check_replay() {
+  if (layout_.nodes <= 1) return;
+  Impl& I = *impl_;
+  for (int k = 0; k < 2; ++k)
+    if (I.host_bad[k] != ~0ULL) {
+      const unsigned long long key = I.host_bad[k];
+      I.host_bad[0] = I.host_bad[1] = ~0ULL;
+      throw_non_finite(k == 0 ? I.send : I.own, key);
+    }
+  transport_.check_async();
 }
 
 bool DeviceReducer::poll(bool wait) {
@@ -1258,7 +1327,7 @@ int DeviceReducer::launches_per_call() const {
   if (impl_->flags & GCX_F_BIG_BUCKETS) ++enc;
   if (impl_->flags & GCX_F_ODD_BUCKETS) ++enc;
   const int odd = (impl_->flags & GCX_F_ODD_BUCKETS) ? 1 : 0;  // generic fold / decode too
-  return 2 * enc + 2 * (1 + odd);
+  return 2 * enc + 2 * (1 + odd) + (impl_->dev_seeds ? 1 : 0);  // + gcx_sra_step_seeds
 }
 
 }  // namespace gcomm::collectives

@@ -371,6 +371,16 @@ class DeviceReducer {
   // wait = false: only if that call has finished on the device (no sync).
   // Returns whether the last call has completed.
   bool poll(bool wait);
+  // Graph-replayable steps: from now on allreduce() ignores step_seed and
+  // takes the step seed H(H(base_seed, step), buffer) (engine.cpp:208-209)
+  // from a device-resident counter that starts at next_step and advances on
+  // the device every call, so a step captured in a CUDA graph (NCCL
+  // transport) replays with fresh keys.  Span tables only.
+  void use_device_seeds(std::uint64_t base_seed, std::uint64_t buffer, std::uint64_t next_step);
+  std::uint64_t device_step() const;  // the counter (synchronous read)
+  // After a captured step's replay has completed: raise its non-finite /
+  // transport errors (poll() covers eager calls).
+  void check_replay();
   std::size_t elements() const { return layout_.d; }
   const SraLayout& layout() const { return layout_; }
   StepTrace trace() const;

@@ -114,6 +114,7 @@ class CompressedAllreduce:
         self._launched = [False] * len(self.buffers)
         self._step = None
         self._origin = None
+        self._dev_next = None  # device-resident seeds: the step the counters hold
 
     @property
     def elements(self) -> int:
@@ -134,9 +135,58 @@ class CompressedAllreduce:
             self._launch(b)
         self.end()
 
+    # -- CUDA-graph form ---------------------------------------------------------
+    def use_device_seeds(self, next_step: int):
+        """Every reducer takes its step seed H(H(step_seed, step), buffer)
+        (engine.cpp:208-209) from a device-resident counter starting at
+        ``next_step`` and advanced on the device per call, so a captured step
+        replays with fresh keys.  Steps must then run consecutively."""
+        self.poll(wait=True)
+        for b, r in enumerate(self.reducers):
+            r.use_device_seeds(self.step_seed, b, next_step)
+        self._dev_next = next_step
+
+    def capture(self, next_step: int, stream=None):
+        """Capture one whole step — every fused buffer's K1, exchange, owner
+        step, exchange and K3 on its own stream — as a CUDA graph.  Each
+        ``graph.replay()`` then averages the fused buffers in place for the
+        next step (next_step, next_step + 1, ...) with no per-kernel host
+        work; call ``check_replay()`` after a replay has completed to raise
+        its non-finite / transport errors.  NCCL transport only (the
+        loopback's rounds are host rendezvous)."""
+        import torch
+        self.use_device_seeds(next_step)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            origin = torch.cuda.current_stream()
+            self._step, self._origin = next_step, origin
+            self._pending = [len(fb.segments) for fb in self.buffers]
+            self._launched = [False] * len(self.buffers)
+            for b in range(len(self.buffers)):
+                self._launch(b)
+            if self.pipeline:
+                for s in self.streams:
+                    origin.wait_stream(s)
+            self._step = None
+        self._dev_next = None  # replays advance the counters on the device
+        return graph
+
+    def check_replay(self):
+        for r in self.reducers:
+            r.check_replay()
+
+    def device_step(self) -> int:
+        """The step the next call / replay reduces (device-resident seeds)."""
+        return self.reducers[0].device_step()
+
     # -- readiness-driven form (size trigger) -----------------------------------
     def begin(self, step: int, stream=None):
         self.poll(wait=True)
+        if self._dev_next is not None:
+            if step != self._dev_next:
+                raise ValueError(f"device-resident seeds hold step {self._dev_next}, "
+                                 f"not {step}: steps must run consecutively")
+            self._dev_next += 1
         self._step = step
         self._origin = stream or torch.cuda.current_stream()
         self._pending = [len(fb.segments) for fb in self.buffers]
