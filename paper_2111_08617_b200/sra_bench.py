@@ -97,6 +97,37 @@ def run(args, metric, ClockSampler, measured_peaks, cpu_sra_sample):
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms = float(te.item())
 
+    # the same step captured once as a CUDA graph (device-resident seeds, both
+    # NCCL rounds inside the graph) and replayed.  Every rank must capture
+    # successfully before any rank replays (a lone replay would wait on
+    # peers that never join), so success is agreed over torch.distributed.
+    graph_ms, graph_err = None, None
+    if os.environ.get("GCX_BENCH_GRAPH", "1") != "0":
+        gr = None
+        try:
+            gr = car.capture(20_000)
+        except Exception as e:  # noqa: BLE001 -- reported in the JSON line
+            graph_err = f"capture: {type(e).__name__}: {e}"[:300]
+        ok = torch.tensor([1 if gr is not None else 0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 1:
+            gr.replay()
+            torch.cuda.synchronize()
+            car.check_replay()
+            dist.barrier()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(args.steps):
+                gr.replay()
+            g1.record(stream)
+            torch.cuda.synchronize()
+            car.check_replay()
+            tg = torch.tensor([g0.elapsed_time(g1) / args.steps], device="cuda")
+            dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+            graph_ms = float(tg.item())
+        elif graph_err is None:
+            graph_err = "another rank failed to capture"
+
     busbw = lambda ms_: (4 * n / (ms_ * 1e-3)) * 2 * (world - 1) / world / 1e9  # noqa: E731
     # the reference's CPU SRA on this host (rank 0 only, after the timed region)
     cb = None
@@ -120,6 +151,12 @@ def run(args, metric, ClockSampler, measured_peaks, cpu_sra_sample):
                        "aggregate_input_GBps": world * 4 * n / (ms * 1e-3) / 1e9,
                        "aggregate_note": "all ranks' gradient bytes reduced per second "
                                          "(N x 4n / t)",
+                       "graph_ms_per_step": graph_ms,
+                       "graph_busbw_GBps": busbw(graph_ms) if graph_ms else None,
+                       "graph_note": "the step captured once as a CUDA graph "
+                                     "(CompressedAllreduce.capture: device-resident seeds, "
+                                     "NCCL rounds in the graph), K back-to-back replays "
+                                     "on resident data" + (f"; {graph_err}" if graph_err else ""),
                        "nccl_fp32_allreduce_ms": base_ms,
                        "nccl_fp32_busbw_GBps": busbw(base_ms),
                        "speedup_vs_nccl_fp32": base_ms / ms,
