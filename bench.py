@@ -417,6 +417,7 @@ def run_codec(args):
     # on this GPU (exchange in device memory): per-rank kernel time, the
     # compute side of the multi-GPU number (scripts/sra_emul_bench.py)
     sra8 = sra_emulation(8)
+    sra8_graph = sra_emulation(8, graph=True)
 
     # end to end through the C-ABI with host buffers: every step copies its
     # input from pinned host memory (H2D), runs gcx_quantize + gcx_dequantize
@@ -463,6 +464,7 @@ def run_codec(args):
                            "each step hashes mix64(seed ^ T(i)) with a fresh seed",
                    "quantize_inline_ms": q_inline_ms,
                    "sra_n8_emulated_per_rank_kernel_ms": sra8,
+                   "sra_n8_emulated_per_rank_graph_ms": sra8_graph,
                    "k4_window_accumulate_ms": acc_ms,
                    "k4_window_accumulate_GBps": 20 * n / (acc_ms * 1e-3) / 1e9,
                    "k4_note": "adaptive statistics: sum[i] += (double)g[i] (read 4+8 B, write 8 B "
@@ -503,11 +505,25 @@ def run_codec(args):
     return 0
 
 
-def sra_emulation(nodes):
+def sra_emulation(nodes, graph=False):
     """Kernel time per rank of one SRA step (ResNet-50 layer list, default
     filter, 4b/128, 64 MiB buffers, average) with all `nodes` ranks' K1 /
-    fold / K3 run on this GPU; best of 3 after a warm-up."""
+    fold / K3 run on this GPU; best of 3 after a warm-up.  graph: the step's
+    kernels captured as a CUDA graph and launched once (GCX_EMUL_GRAPH), so
+    host launch gaps between dependent kernels drop out."""
     import numpy as np
+    prev = os.environ.get("GCX_EMUL_GRAPH")
+    os.environ["GCX_EMUL_GRAPH"] = "1" if graph else "0"
+    try:
+        return _sra_emulation(nodes, np)
+    finally:
+        if prev is None:
+            os.environ.pop("GCX_EMUL_GRAPH", None)
+        else:
+            os.environ["GCX_EMUL_GRAPH"] = prev
+
+
+def _sra_emulation(nodes, np):
 
     from paper_2111_08617_b200 import _gcomm as G
     from paper_2111_08617_b200.ddp import load_layout, resolve_codecs

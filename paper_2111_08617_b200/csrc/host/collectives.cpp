@@ -339,6 +339,60 @@ struct TableBlob {
   }
 };
 
+// Device time of the kernels issued between construction and end_ms() on
+// st (the single-GPU drivers' device_time_s).  GCX_EMUL_GRAPH=1 captures
+// the region as a CUDA graph and launches it once, so the events bracket
+// device work only -- what a graph-replayed per-rank step runs
+// (DeviceReducer::use_device_seeds); by default the region is timed as
+// issued, host launch gaps included.
+struct TimedRegion {
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  bool graph;
+  explicit TimedRegion(cudaStream_t s) : st(s) {
+    const char* e = std::getenv("GCX_EMUL_GRAPH");
+    graph = e != nullptr && e[0] == '1';
+    cuda_check(cudaEventCreate(&e0), "event");
+    cuda_check(cudaEventCreate(&e1), "event");
+    if (graph)
+      cuda_check(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed), "begin capture");
+    else
+      cuda_check(cudaEventRecord(e0, st), "event record");
+  }
+  float end_ms() {
+    if (graph) {
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t ge = nullptr;
+      cuda_check(cudaStreamEndCapture(st, &g), "end capture");
+      cuda_check(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+      cuda_check(cudaGraphUpload(ge, st), "graph upload");
+      cuda_check(cudaEventRecord(e0, st), "event record");
+      cuda_check(cudaGraphLaunch(ge, st), "graph launch");
+      cuda_check(cudaEventRecord(e1, st), "event record");
+      cuda_check(cudaStreamSynchronize(st), "sync");
+      cudaGraphExecDestroy(ge);
+      cudaGraphDestroy(g);
+    } else {
+      cuda_check(cudaEventRecord(e1, st), "event record");
+      cuda_check(cudaEventSynchronize(e1), "sync");
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return ms;
+  }
+  ~TimedRegion() {
+    cudaStreamCaptureStatus c = cudaStreamCaptureStatusNone;
+    if (graph && cudaStreamIsCapturing(st, &c) == cudaSuccess && c != cudaStreamCaptureStatusNone) {
+      cudaGraph_t g = nullptr;  // an exception left the capture open: close and drop it
+      if (cudaStreamEndCapture(st, &g) == cudaSuccess && g) cudaGraphDestroy(g);
+    }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+  }
+  TimedRegion(const TimedRegion&) = delete;
+  TimedRegion& operator=(const TimedRegion&) = delete;
+};
+
 // K1 over a table quantized under one seed: draw the shared key runs once
 // (gcx_make_keys), then norms + quantize + pack reading keys from the table
 // (from the table's stored key prefixes when given: one finalizer per slot)
@@ -839,10 +893,7 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
                                     tt[r]->key_len, kpre[2 * k + r].get<unsigned long long>(), st));
     }
   }
-  cudaEvent_t e0, e1;
-  cuda_check(cudaEventCreate(&e0), "event");
-  cuda_check(cudaEventCreate(&e1), "event");
-  cudaEventRecord(e0, st);
+  TimedRegion timed(st);
   auto* badp = bad.get<unsigned long long>();
   auto* kp = keys.get<unsigned long long>();
   const float divisor = req.op == ReduceOp::average ? float(N) : 1.0f;
@@ -863,7 +914,7 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
                                 std::uint32_t(dec[id].pieces.size()), dec[id].ntiles,
                                 dec[id].flags, gather.get<std::uint8_t>(),
                                 out.get<float>() + id * d, divisor, st));
-  cudaEventRecord(e1, st);
+  const float ms = timed.end_ms();
   result.outputs.assign(N, std::vector<float>(d));
   for (std::size_t k = 0; k < N; ++k)
     cuda_check(cudaMemcpyAsync(result.outputs[k].data(), out.get<float>() + k * d, 4 * d,
@@ -871,10 +922,6 @@ ReduceResult allreduce(const ReduceRequest& req, std::size_t nodes) {
   std::vector<std::uint64_t> badh(2 * N);
   cuda_check(cudaMemcpyAsync(badh.data(), bad.get(), 16 * N, cudaMemcpyDeviceToHost, st), "D2H");
   stream.sync();
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   for (std::size_t k = 0; k < 2 * N; ++k)
     if (badh[k] != ~0ULL) throw_non_finite(k < N ? send[k] : own[k - N], badh[k]);
   result.trace = sra_trace(L);

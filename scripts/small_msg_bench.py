@@ -1,7 +1,8 @@
 """Small-message SRA (BASELINE config 5's low end) on one GPU: per-rank kernel
 time of one compressed allreduce, every rank's kernels on this B200, for
 64 KiB .. 4 MiB at N = 2/4/8, 4 bits (scripts/sweep_c5.py's measurement on a
-short size list).  Development / evidence tool (GPU box)."""
+short size list).  GCX_EMUL_GRAPH=1: the step's kernels are launched as one
+CUDA graph (device work only).  Development / evidence tool (GPU box)."""
 import os
 import sys
 
