@@ -157,7 +157,9 @@ class CompressedAllreduce:
         import torch
         self.use_device_seeds(next_step)
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
+        # thread-local capture mode: other threads (NCCL's proxy, torch's
+        # process-group watchdog) keep querying their events meanwhile
+        with torch.cuda.graph(graph, stream=stream, capture_error_mode="thread_local"):
             origin = torch.cuda.current_stream()
             self._step, self._origin = next_step, origin
             self._pending = [len(fb.segments) for fb in self.buffers]

@@ -104,6 +104,8 @@ def run(args, metric, ClockSampler, measured_peaks, cpu_sra_sample):
     graph_ms, graph_err = None, None
     if os.environ.get("GCX_BENCH_GRAPH", "1") != "0":
         gr = None
+        torch.cuda.synchronize()  # no process-group work in flight during the capture
+        dist.barrier()
         try:
             gr = car.capture(20_000)
         except Exception as e:  # noqa: BLE001 -- reported in the JSON line
