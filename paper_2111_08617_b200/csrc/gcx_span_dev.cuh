@@ -1375,7 +1375,113 @@ constexpr int kFoldWarps = 4;
 // FOLD = false is the same CTA-per-tile K1 fed from `src` (phase A stages
 // rows 8w..8w+7 by coalesced loads): the small-message form of k_span_pieces,
 // whose one-warp tiles leave a short table latency-bound (bucket 128 only).
-template <uint32_t BITS, int LGB, int KM, bool FOLD>
+#ifndef GCX_FOLD_PEER_MAJOR
+#define GCX_FOLD_PEER_MAJOR 4  // node counts up to this take the peer-major fold (widths <= 4)
+#endif
+// The CTA owner step's fold (widths <= 4) peer-major: a warp's 8 rows
+// (warp, warp + 4, ...), in two passes of 4, are folded one peer at a time in
+// ascending node id (collectives.cpp:268-279; the owner's raw quads at id ==
+// me), so a peer's receive slot is addressed once per pass, its 4 rows'
+// norms and packed windows are loaded together (12 independent loads), and
+// the next peer's loads are in flight while this peer is decoded.  Per row and peer: the
+// lane's table entry (one FP64 dequant_field evaluation) and four shuffles.
+template <uint32_t BITS, int LGB>
+__device__ __forceinline__ void fold_rows_peer_major(const SpanPiecesArgs& A, const gcx_piece& p,
+                                                     uint32_t start, uint32_t count, float* slots,
+                                                     uint32_t lane, uint32_t warp) {
+  constexpr uint32_t W = BITS + 1, S = (1u << BITS) - 1, F = 2u << BITS;
+  constexpr uint32_t RB = 16u / kFoldWarps;  // rows per pass (two passes: 8 rows per warp)
+  const uint32_t f = lane & (F - 1u), level = f & S, sign = f >> BITS;
+  const double dl = double(level);
+  const double sd = double(S), ys = __drcp_rn(sd);
+  const uint32_t qbit = 4 * W * lane, qw = qbit >> 5, qsh = qbit & 31u;
+  const bool two = qsh + 4 * W > 32;
+  const uint32_t nodes = A.nodes, me = A.me;
+  struct PeerLoads {
+    uint32_t nu[RB], w0[RB], w1[RB];
+  };
+#pragma unroll 1
+  for (uint32_t half = 0; half < 2; ++half) {
+  const uint32_t w0r = warp + half * RB * kFoldWarps;  // this pass's first row
+  auto vrow = [&](uint32_t j) {
+    const uint32_t r = w0r + j * kFoldWarps;
+    return count > r * 128u ? min(128u, count - r * 128u) : 0u;
+  };
+  auto load_peer = [&](uint32_t id, PeerLoads& L) {
+    const uint8_t* m = A.recv + uint64_t(id < me ? id : id - 1) * A.slot_stride;
+    const uint32_t* nb = reinterpret_cast<const uint32_t*>(m + p.norms);
+    const uint32_t* wb = reinterpret_cast<const uint32_t*>(m + p.packed) + qw;
+#pragma unroll
+    for (uint32_t j = 0; j < RB; ++j) {
+      const uint32_t vr = vrow(j);
+      const uint32_t e_row = start + (w0r + j * kFoldWarps) * 128u;
+      L.nu[j] = vr > 0 ? __ldg(nb + (e_row >> LGB)) : 0u;
+      const bool quad = 4 * lane < vr;
+      L.w0[j] = quad ? __ldg(wb + (e_row >> 5) * W) : 0u;
+      L.w1[j] = quad && two ? __ldg(wb + (e_row >> 5) * W + 1) : 0u;
+    }
+  };
+  float acc[RB][4];
+  PeerLoads cur, nxt;
+  const uint32_t first = me == 0 ? 1u : 0u;
+  load_peer(first, cur);
+#pragma unroll
+  for (uint32_t id = 0; id < 8; ++id) {
+    if (id >= nodes) break;
+    if (id == me) {  // the owner's raw values
+#pragma unroll
+      for (uint32_t j = 0; j < RB; ++j) {
+        const uint32_t vr = vrow(j);
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (4 * lane < vr) {
+          const float* o = A.src + p.src + start + (w0r + j * kFoldWarps) * 128u + 4 * lane;
+          if (4 * lane + 4 <= vr && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
+            v = __ldg(reinterpret_cast<const float4*>(o));
+          } else {
+            v.x = __ldg(o);
+            if (4 * lane + 1 < vr) v.y = __ldg(o + 1);
+            if (4 * lane + 2 < vr) v.z = __ldg(o + 2);
+            if (4 * lane + 3 < vr) v.w = __ldg(o + 3);
+          }
+        }
+        const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[j][k] = id == 0 ? x[k] : __fadd_rn(acc[j][k], x[k]);
+      }
+      continue;
+    }
+    const uint32_t nid = id + 1 == me ? id + 2 : id + 1;
+    if (nid < nodes) load_peer(nid, nxt);
+#pragma unroll
+    for (uint32_t j = 0; j < RB; ++j) {
+      // this lane's entry of the peer's table for row j's bucket (dequant_field)
+      const double nl = __dmul_rn(double(__uint_as_float(cur.nu[j])), dl);  // exact
+      const double q0 = __dmul_rn(nl, ys);
+      const double q = __fma_rn(__fma_rn(-sd, q0, nl), ys, q0);
+      const float mg = __double2float_rn(q);
+      const float entry = level == 0 ? 0.0f : (sign ? -mg : mg);
+      const uint32_t win = two ? __funnelshift_r(cur.w0[j], cur.w1[j], qsh) : (cur.w0[j] >> qsh);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float x = __shfl_sync(0xffffffffu, entry, (win >> (k * W)) & (F - 1u));
+        acc[j][k] = id == 0 ? x : __fadd_rn(acc[j][k], x);
+      }
+    }
+    cur = nxt;
+  }
+#pragma unroll
+  for (uint32_t j = 0; j < RB; ++j) {
+    const uint32_t r = w0r + j * kFoldWarps, vr = vrow(j);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (4 * lane + k >= vr) acc[j][k] = 0.0f;  // past the piece: the zero-filled tile
+    float* dst = slots + (lane >> 3) * kSlotFloats + r * 32u + (((lane & 7u) ^ (r & 7u)) << 2);
+    *reinterpret_cast<float4*>(dst) = make_float4(acc[j][0], acc[j][1], acc[j][2], acc[j][3]);
+  }
+  }  // half
+}
+
+template <uint32_t BITS, int LGB, int KM, bool FOLD, bool PM = false>
 __global__ void __launch_bounds__(32 * kFoldWarps, GCX_FOLD_MINB) k_span_fold_cta(SpanPiecesArgs A) {
   constexpr uint32_t W = BITS + 1;
   extern __shared__ __align__(1024) unsigned char span_smem[];
@@ -1425,7 +1531,12 @@ __global__ void __launch_bounds__(32 * kFoldWarps, GCX_FOLD_MINB) k_span_fold_ct
     // A: fold (or stage) rows 8w..8w+7
     if constexpr (FOLD) {
       // rows warp, warp+4, ...: a short tile's rows spread over all four warps
-      fold_tile<BITS, LGB>(A, p, cur.start, cur.count, slots, lane, warp, 32, kFoldWarps);
+      // PM (few peers, widths <= 4): peer-major; else the row-major fold with
+      // its one-row-ahead loads (faster at N = 8)
+      if constexpr (PM && (2u << BITS) <= 32)
+        fold_rows_peer_major<BITS, LGB>(A, p, cur.start, cur.count, slots, lane, warp);
+      else
+        fold_tile<BITS, LGB>(A, p, cur.start, cur.count, slots, lane, warp, 32, kFoldWarps);
     } else {
       const float* xs = A.src + p.src + cur.start;
       const bool al = (reinterpret_cast<uintptr_t>(A.src + p.src) & 15u) == 0;

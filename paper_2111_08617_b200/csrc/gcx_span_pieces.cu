@@ -48,7 +48,26 @@ static SpanPiecesFn pick_fold_lgb(int bits, bool prefix) {
   }
 }
 
-static SpanPiecesFn pick_fold(int bits, int lgb, bool prefix) {
+// the peer-major fold (few peers, widths <= 4)
+template <int LGB>
+static SpanPiecesFn pick_fold_pm_lgb(int bits, bool prefix) {
+  switch (bits) {
+    case 1: return prefix ? k_span_fold_cta<1, LGB, kKmPrefix, true, true> : k_span_fold_cta<1, LGB, kKmInline, true, true>;
+    case 2: return prefix ? k_span_fold_cta<2, LGB, kKmPrefix, true, true> : k_span_fold_cta<2, LGB, kKmInline, true, true>;
+    case 3: return prefix ? k_span_fold_cta<3, LGB, kKmPrefix, true, true> : k_span_fold_cta<3, LGB, kKmInline, true, true>;
+    case 4: return prefix ? k_span_fold_cta<4, LGB, kKmPrefix, true, true> : k_span_fold_cta<4, LGB, kKmInline, true, true>;
+    default: return nullptr;
+  }
+}
+
+static SpanPiecesFn pick_fold(int bits, int lgb, bool prefix, bool pm) {
+  if (pm && GCX_FOLD_CTA && bits <= 4) {
+    switch (lgb) {
+      case 7: return pick_fold_pm_lgb<7>(bits, prefix);
+      case 9: return pick_fold_pm_lgb<9>(bits, prefix);
+      default: return nullptr;
+    }
+  }
   switch (lgb) {
     case 7: return pick_fold_lgb<7>(bits, prefix);
     case 9: return pick_fold_lgb<9>(bits, prefix);
@@ -209,14 +228,15 @@ cudaError_t gcx_span_fold_encode(const gcx_piece* pieces, const uint32_t* tile_p
   if (!gcx_span_fold_ok(flags, nodes) || me >= nodes) return cudaErrorInvalidValue;
   const int bits = int((flags >> GCX_F_SPAN_BITS_SHIFT) & 15u);
   const int lgb = int((flags >> GCX_F_SPAN_LGB_SHIFT) & 15u);
-  SpanPiecesFn fn = pick_fold(bits, lgb, prefix != nullptr);
+  const bool pm = nodes <= GCX_FOLD_PEER_MAJOR && bits <= 4;
+  SpanPiecesFn fn = pick_fold(bits, lgb, prefix != nullptr, pm);
   if (fn == nullptr) return cudaErrorInvalidValue;
   const uint32_t W = uint32_t(bits) + 1;
   const size_t smem = GCX_FOLD_CTA ? size_t(4 * kSlotFloats * 4 + out_words(W) * 4 + 64 * 4)
                                    : size_t(kWarps) * warp_smem_bytes(W);
   const int threads = GCX_FOLD_CTA ? 32 * kFoldWarps : 32 * kWarps;
-  static thread_local int occ[9][13][2] = {};
-  int& o = occ[bits][lgb][prefix != nullptr];
+  static thread_local int occ[9][13][2][2] = {};
+  int& o = occ[bits][lgb][prefix != nullptr][pm];
   if (o == 0) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
