@@ -425,6 +425,7 @@ def run_codec(args):
     # streams (copy-in, compute, copy-out) so step k's D2H overlaps step k+1's
     # H2D on the two copy engines, as a streaming caller would run it.
     e2e_ms = e2e_codec(args, sets, n, bits, bucket)
+    pcie = pcie_copy_rates(sets, n)
     peak, peak_kind = measured_peaks()
     q_bytes = 4 * n + compressed_bytes(n, bits, bucket)
     achieved = q_bytes / (q_ms * 1e-3) / 1e9
@@ -497,7 +498,11 @@ def run_codec(args):
                                             "cpu_model")},
         "e2e": {"value": 4 * n / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
                 "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n,
-                "path": "pinned H2D -> gcx_quantize_prefixed -> gcx_dequantize -> D2H, steps double-buffered over copy-in / compute / copy-out streams"},
+                "path": "pinned H2D -> gcx_quantize_prefixed -> gcx_dequantize -> D2H, steps double-buffered over copy-in / compute / copy-out streams",
+                # the e2e roofline: the same pinned copies with no compute,
+                # both directions at once (what one e2e step must move)
+                "pcie_copy_GBps": pcie,
+                "frac_of_copy_only": (4 * n / (e2e_ms * 1e-3) / 1e9) / pcie["bidir_per_direction"]},
         "gpu_launches": 2 * args.steps,  # k_span + k_dspan per step
         "clocks": clk.summary(),
     }
@@ -544,6 +549,38 @@ def _sra_emulation(nodes, np):
         G.allreduce(req, nodes)
         total += min(G.allreduce(req, nodes).trace.device_time_s for _ in range(3))
     return total * 1e3 / nodes
+
+
+def pcie_copy_rates(sets, n, reps=5):
+    """Pinned host<->device copy rates of one C1 gradient (4n bytes): H2D
+    alone, D2H alone, and both at once on two streams (GB/s per direction),
+    best of `reps`.  The ceiling of the e2e leg, which moves 4n each way per
+    step."""
+    import torch
+    hx = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    hy = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    a, b = sets[0][0], sets[1][3]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn):
+        best = 1e30
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        return 4 * n / best / 1e9
+
+    def both():
+        with torch.cuda.stream(s1):
+            a.copy_(hx, non_blocking=True)
+        with torch.cuda.stream(s2):
+            hy.copy_(b, non_blocking=True)
+
+    return {"h2d": timed(lambda: a.copy_(hx, non_blocking=True)),
+            "d2h": timed(lambda: hy.copy_(b, non_blocking=True)),
+            "bidir_per_direction": timed(both)}
 
 
 def e2e_codec(args, sets, n, bits, bucket):
