@@ -429,6 +429,7 @@ def run_codec(args):
     peak, peak_kind = measured_peaks()
     q_bytes = 4 * n + compressed_bytes(n, bits, bucket)
     achieved = q_bytes / (q_ms * 1e-3) / 1e9
+    step_bytes = 8 * n + 8 * int(prefix.numel()) + 2 * compressed_bytes(n, bits, bucket)
     cb = cpu_codec_sample(reps=3)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "round2_c1_k_span.json")
@@ -471,6 +472,12 @@ def run_codec(args):
                    "k4_note": "adaptive statistics: sum[i] += (double)g[i] (read 4+8 B, write 8 B "
                               "per element), once per step inside observation windows",
                    "quantize_GBps_algorithmic": achieved,
+                   # what one step must move through HBM with the prefix
+                   # design: K1 reads x (4n) and the key prefixes (8 B per
+                   # slot), writes the message; K3 reads it, writes 4n
+                   "step_hbm_bytes": step_bytes,
+                   "step_hbm_GBps": step_bytes / (ms * 1e-3) / 1e9,
+                   "step_hbm_frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
                    "dequantize_GBps_algorithmic": q_bytes / (dq_ms * 1e-3) / 1e9,
                    "dequantize_roofline_frac": q_bytes / (dq_ms * 1e-3) / 1e9 / peak,
                    "dequantize_kernel": "k_dspan<4,7> (K3: per-lane shuffle tables, "
@@ -485,14 +492,17 @@ def run_codec(args):
                                "one SplitMix64 finalizer per element from the key prefixes, "
                                "register bit-packing, bulk-stored words; one launch per "
                                "gcx_quantize_prefixed)", "peak_kind": peak_kind,
-                     "note": "K1 is bound by instruction issue and latency, not HBM: ~43 "
-                             "instructions per element (the reference RNG's finalizer ~18, "
-                             "exact FP64 level arithmetic, packing) at 2 warps per scheduler "
-                             "(216 registers); it reads the 8-byte prefix T(i) per element "
-                             "(traffic ~ 4+8 B/elem vs 4.66 algorithmic).  The bit-exact "
-                             "contract (SURVEY Appendix B) rules out skipping the hash; "
-                             "config.hash_only_ms is the three-finalizer hash alone.  ncu: "
-                             "profiles/round2_c1_k_span.md",
+                     "note": "frac counts K1's algorithmic bytes (x in, message out: 4.66 B/elem). "
+                             "K1 also reads the 8-byte key prefix T(i) per element (the "
+                             "seed-independent half of the reference RNG, built once per "
+                             "buffer shape), so its DRAM traffic is ~12.5 B/elem (traffic, "
+                             "from ncu): 320 MB per launch, 4.4-5.2 TB/s at 62-73 us -- "
+                             "67-79 % of HBM on the bytes it must move.  The C1 step as a "
+                             "whole moves config.step_hbm_bytes at config.step_hbm_frac of "
+                             "HBM.  Hashing the prefixes inline instead costs two more "
+                             "SplitMix64 finalizers per element (config.quantize_inline_ms, "
+                             "config.hash_only_ms); the bit-exact contract (SURVEY Appendix B) "
+                             "rules out skipping the hash.  ncu: profiles/round2_c1_k_span.md",
                      "algorithmic_bytes_per_launch": q_bytes},
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
                                             "cpu_model")},
